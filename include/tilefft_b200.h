@@ -1,0 +1,115 @@
+/* tilefft_b200 — C ABI of the B200-native complex-to-complex FFT path.
+ *
+ * This is the drop-in boundary below the reference's C++ plan/execute API
+ * (/root/reference/proj/include/tilefft). The reference has no FFI of its own
+ * (SURVEY §8b): its public entry points are header templates, so the C++
+ * headers in include/tilefft/ keep those signatures and call these functions.
+ * Each entry point cites the reference interface it replaces.
+ *
+ * Conventions: plain pointers and sizes only; complex data is interleaved
+ * (re, im) — the layout of std::vector<std::complex<Real>> — in fp32
+ * (elem_bytes = 8) or fp64 (elem_bytes = 16). Every call returns 0 or a
+ * TILEFFT_E* code and never throws; tilefft_last_error() holds the message
+ * (thread-local), using the reference's wording where the reference has one
+ * (detail::require, common.hpp:47-51). There is no CPU fallback: without a
+ * CUDA device every call fails with TILEFFT_ENODEV.
+ */
+#ifndef TILEFFT_B200_H
+#define TILEFFT_B200_H
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TILEFFT_API __attribute__((visibility("default")))
+#else
+#define TILEFFT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TILEFFT_OK 0
+#define TILEFFT_EINVAL 22  /* maps to std::invalid_argument */
+#define TILEFFT_ENODEV 19  /* no usable sm_100 device */
+#define TILEFFT_ENOMEM 12
+#define TILEFFT_ECUDA 1001 /* CUDA runtime error (message in tilefft_last_error) */
+#define TILEFFT_ENCCL 1002
+
+/* Arithmetic modes.
+ *  FAST  : the product path. Radix-32 register Stockham passes over the
+ *          GPU's own pass factorisation; relative L2 error vs fft_tiled
+ *          <= 1e-5*log2(N) (fp32) / 1e-12*log2(N) (fp64).
+ *  EXACT : executes the caller's plan factors with the reference's radix-2
+ *          dataflow and table roots, every op separately rounded: output is
+ *          bit-identical to fft_tiled<Real> (tiled_fft.hpp:321-407).
+ *  PERMUTE (EXACT only): butterflies and roots off; applies only the pass
+ *          index maps (gather/exchange/interleave, stage_plan.hpp:135-179). */
+#define TILEFFT_MODE_FAST 0
+#define TILEFFT_MODE_EXACT 1
+#define TILEFFT_MODE_PERMUTE 2
+
+#define TILEFFT_FORWARD (-1)
+#define TILEFFT_INVERSE (+1)
+
+typedef struct tilefft_plan_s* tilefft_plan_t;
+
+/* Create a plan for `batch` contiguous length-n transforms on `device`.
+ * Replaces make_plan (stage_plan.hpp:74-127) + build_twiddle_table
+ * (twiddle.hpp:47-73) as consumed by fft_tiled: `factors` are the
+ * StagePlan's factors (required for EXACT/PERMUTE, advisory for FAST);
+ * `twiddle_values`/`twiddle_resolution` are the caller's TwiddleTable
+ * (interleaved, elem_bytes each) — EXACT mode takes its roots from it; pass
+ * NULL/0 to have the plan generate the same values itself.
+ * Errors mirror fft_tiled's checks (tiled_fft.hpp:325-333). */
+TILEFFT_API int tilefft_plan_create(tilefft_plan_t* plan, uint64_t n, uint64_t batch, const uint64_t* factors,
+                        uint32_t nfactors, uint32_t elem_bytes, uint32_t mode, const void* twiddle_values,
+                        uint64_t twiddle_resolution, int device);
+
+/* 2D transform of `batch` row-major ny x nx images (rows then columns; the
+ * reference has no 2D entry point — SPEC.md:331 — so this composes the 1D
+ * passes exactly as the BASELINE.md recipe does). FAST mode only. */
+TILEFFT_API int tilefft_plan_create_2d(tilefft_plan_t* plan, uint64_t ny, uint64_t nx, uint64_t batch, uint32_t elem_bytes,
+                           int device);
+
+/* Execute on device-resident buffers (out-of-place; in == out allowed).
+ * sign = TILEFFT_FORWARD is fft_tiled (tiled_fft.hpp:321); TILEFFT_INVERSE
+ * is ifft_tiled (:410-423), including the 1/n scale. Asynchronous on
+ * `cuda_stream` (a cudaStream_t; NULL = legacy default stream). */
+TILEFFT_API int tilefft_exec_c2c(tilefft_plan_t plan, const void* d_in, void* d_out, int sign, void* cuda_stream);
+
+/* Execute on HOST buffers: the whole fft_tiled contract (vector in, vector
+ * out). Host->device copies, the passes and device->host copies are
+ * pipelined in chunks of transforms over several streams when batch > 1.
+ * Synchronous. Pinned (cudaHostAlloc/registered) buffers reach full PCIe
+ * bandwidth; pageable buffers work but are staged by the driver. */
+TILEFFT_API int tilefft_exec_c2c_host(tilefft_plan_t plan, const void* h_in, void* h_out, int sign);
+
+TILEFFT_API int tilefft_plan_destroy(tilefft_plan_t plan);
+
+/* Plan introspection (all sizes in elements unless noted). */
+typedef struct {
+  uint64_t n, batch, ny, nx;
+  uint32_t elem_bytes, mode, is_2d;
+  uint32_t passes;             /* device passes per transform (HBM round trips) */
+  uint64_t factors[16];        /* device pass lengths in execution order */
+  uint32_t launches_per_exec;  /* kernel launches per tilefft_exec_c2c */
+  uint64_t workspace_bytes;    /* device scratch held by the plan */
+  uint64_t table_bytes;        /* device twiddle tables held by the plan */
+} tilefft_plan_info_t;
+TILEFFT_API int tilefft_plan_info(tilefft_plan_t plan, tilefft_plan_info_t* info);
+
+/* Host-side root table with the reference's construction: entry j =
+ * exp(-2 pi i j / resolution), interleaved, elem_bytes 8 or 16
+ * (build_twiddle_table, twiddle.hpp:47-73; bit-identical values). */
+TILEFFT_API int tilefft_build_twiddle(uint64_t resolution, uint32_t elem_bytes, void* out);
+
+/* Thread-local message of the last failing call ("" if none). */
+TILEFFT_API const char* tilefft_last_error(void);
+
+/* Library version / build string, e.g. "tilefft_b200 0.1 sm_100a". */
+TILEFFT_API const char* tilefft_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,168 @@
+"""ctypes binding of the C ABI in include/tilefft_b200.h.
+
+Loads the in-tree ``libtilefft_b200.so`` (built by ``__graft_entry__.build()`` /
+``make -C paper_1707_07263_b200/csrc``). There is deliberately no fallback: if
+the library is missing, or no sm_100 device is present when a plan is created,
+the call raises — the product path never runs on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtilefft_b200.so")
+
+OK = 0
+EINVAL = 22
+ENODEV = 19
+ENOMEM = 12
+ECUDA = 1001
+ENCCL = 1002
+
+MODE_FAST = 0
+MODE_EXACT = 1
+MODE_PERMUTE = 2
+FORWARD = -1
+INVERSE = +1
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_uint64),
+        ("batch", ctypes.c_uint64),
+        ("ny", ctypes.c_uint64),
+        ("nx", ctypes.c_uint64),
+        ("elem_bytes", ctypes.c_uint32),
+        ("mode", ctypes.c_uint32),
+        ("is_2d", ctypes.c_uint32),
+        ("passes", ctypes.c_uint32),
+        ("factors", ctypes.c_uint64 * 16),
+        ("launches_per_exec", ctypes.c_uint32),
+        ("workspace_bytes", ctypes.c_uint64),
+        ("table_bytes", ctypes.c_uint64),
+    ]
+
+
+# Every symbol include/tilefft_b200.h declares (tests check the exports).
+EXPORTS = (
+    "tilefft_plan_create",
+    "tilefft_plan_create_2d",
+    "tilefft_exec_c2c",
+    "tilefft_exec_c2c_host",
+    "tilefft_plan_destroy",
+    "tilefft_plan_info",
+    "tilefft_build_twiddle",
+    "tilefft_last_error",
+    "tilefft_version",
+)
+
+_lib = None
+_lock = threading.Lock()
+
+
+class TilefftError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+        self.msg = msg
+
+
+def load() -> ctypes.CDLL:
+    """Load the CUDA library (raises if it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(the B200 path has no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        u64, u32, i32, vp = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_void_p
+        lib.tilefft_plan_create.argtypes = [ctypes.POINTER(vp), u64, u64, ctypes.POINTER(u64), u32, u32, u32, vp,
+                                            u64, i32]
+        lib.tilefft_plan_create_2d.argtypes = [ctypes.POINTER(vp), u64, u64, u64, u32, i32]
+        lib.tilefft_exec_c2c.argtypes = [vp, vp, vp, i32, vp]
+        lib.tilefft_exec_c2c_host.argtypes = [vp, vp, vp, i32]
+        lib.tilefft_plan_destroy.argtypes = [vp]
+        lib.tilefft_plan_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
+        lib.tilefft_build_twiddle.argtypes = [u64, u32, vp]
+        lib.tilefft_last_error.restype = ctypes.c_char_p
+        lib.tilefft_version.restype = ctypes.c_char_p
+        for name in ("tilefft_plan_create", "tilefft_plan_create_2d", "tilefft_exec_c2c", "tilefft_exec_c2c_host",
+                     "tilefft_plan_destroy", "tilefft_plan_info", "tilefft_build_twiddle"):
+            getattr(lib, name).restype = ctypes.c_int
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc != OK:
+        msg = load().tilefft_last_error().decode()
+        if rc == EINVAL:
+            # the reference throws std::invalid_argument (common.hpp:47-51)
+            raise ValueError(msg)
+        raise TilefftError(rc, msg)
+
+
+class DevicePlan:
+    """Owning wrapper of a ``tilefft_plan_t``."""
+
+    def __init__(self, handle: int, lib: ctypes.CDLL):
+        self._h = ctypes.c_void_p(handle)
+        self._lib = lib
+
+    @classmethod
+    def create(cls, n, batch=1, factors=None, elem_bytes=8, mode=MODE_FAST, table=None, device=0):
+        lib = load()
+        h = ctypes.c_void_p()
+        fac = None
+        nf = 0
+        if factors:
+            nf = len(factors)
+            fac = (ctypes.c_uint64 * nf)(*[int(f) for f in factors])
+        tv, tres = None, 0
+        if table is not None:
+            tv = ctypes.c_void_p(table.values.ctypes.data)
+            tres = int(table.resolution)
+        check(lib.tilefft_plan_create(ctypes.byref(h), int(n), int(batch), fac, nf, int(elem_bytes), int(mode), tv,
+                                      tres, int(device)))
+        return cls(h.value, lib)
+
+    @classmethod
+    def create_2d(cls, ny, nx, batch=1, elem_bytes=8, device=0):
+        lib = load()
+        h = ctypes.c_void_p()
+        check(lib.tilefft_plan_create_2d(ctypes.byref(h), int(ny), int(nx), int(batch), int(elem_bytes), int(device)))
+        return cls(h.value, lib)
+
+    def exec_device(self, d_in: int, d_out: int, sign: int = FORWARD, stream: int = 0) -> None:
+        check(self._lib.tilefft_exec_c2c(self._h, ctypes.c_void_p(d_in), ctypes.c_void_p(d_out), int(sign),
+                                         ctypes.c_void_p(stream)))
+
+    def exec_host(self, h_in: int, h_out: int, sign: int = FORWARD) -> None:
+        check(self._lib.tilefft_exec_c2c_host(self._h, ctypes.c_void_p(h_in), ctypes.c_void_p(h_out), int(sign)))
+
+    def info(self) -> dict:
+        pi = PlanInfo()
+        check(self._lib.tilefft_plan_info(self._h, ctypes.byref(pi)))
+        d = {k: getattr(pi, k) for k, _ in PlanInfo._fields_ if k != "factors"}
+        d["factors"] = [int(pi.factors[i]) for i in range(pi.passes)]
+        return d
+
+    def close(self) -> None:
+        if self._h and self._h.value:
+            self._lib.tilefft_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_twiddle(resolution: int, elem_bytes: int, out_ptr: int) -> None:
+    check(load().tilefft_build_twiddle(int(resolution), int(elem_bytes), ctypes.c_void_p(out_ptr)))

@@ -1,0 +1,391 @@
+// Fast-mode pass kernels (fp32 / fp64), sm_100a.
+//
+// The reference's pass (tiled_fft.hpp:229-310: gather a decimated comb into a
+// fast tile, run the row butterflies, scale by the inter-pass root and scatter
+// through the pass's store map) is re-derived here as ONE kernel per pass:
+//
+//   * each length-L row FFT is a self-sorting Stockham network whose stages
+//     are radix-32 DFTs held in one thread's registers (fft_common.cuh), so a
+//     1024-point row needs exactly one shared-memory exchange and a 8192-point
+//     row two — instead of the reference's 10/13 radix-2 levels in fast
+//     storage (dit_levels, tiled_fft.hpp:89-117);
+//   * the exchange buffer is padded one slot per 32 (the paper's 16x33 layout,
+//     PAPER.md:200-202, at 8-byte words): every warp-wide access is
+//     bank-conflict free;
+//   * Stockham stage roots come from a per-plan table laid out [q][k] so a
+//     warp's 32 lanes read 32 consecutive entries (read-only path, L1-resident);
+//   * the inter-pass root W_M^{r k} (tiled_fft.hpp:284-294) is fused into the
+//     store and served from a two-level table (coarse x fine, each ~sqrt(M)
+//     entries) instead of the reference's M-entry table;
+//   * strided passes process 16 adjacent combs per CTA so every global access
+//     is a full 128-byte line (measured: 8-byte-wide comb access runs at 15%
+//     of copy bandwidth, 128-byte at 88%; profiles/r01_membench.txt).
+#pragma once
+#include "fft_common.cuh"
+
+namespace tfb {
+
+// ------------------------------------------------------------------ shapes
+// L = T * R: T threads per FFT, R elements per thread; stages radix RMAX
+// except a smaller last one.
+template <int L, int RMAX>
+struct Shape {
+  static constexpr int LOG = ilog2c(L);
+  static constexpr int LR = ilog2c(RMAX);
+  static constexpr int R = L < RMAX ? L : RMAX;
+  static constexpr int T = L / R;
+  static constexpr int NFULL = LOG / LR;
+  static constexpr int LAST = LOG % LR;
+  static constexpr int NST = (L <= RMAX) ? 1 : NFULL + (LAST ? 1 : 0);
+  __host__ __device__ static constexpr int radix(int s) {
+    return (L <= RMAX) ? L : (s < NFULL ? RMAX : (1 << LAST));
+  }
+  __host__ __device__ static constexpr int ns(int s) {
+    int n = 1;
+    for (int i = 0; i < s; ++i) n *= radix(i);
+    return n;
+  }
+  // offset of stage s's [q][k] root table inside this L's table block
+  __host__ __device__ static constexpr int tw_off(int s) {
+    int o = 0;
+    for (int i = 1; i < s; ++i) o += radix(i) * ns(i);
+    return o;
+  }
+  static constexpr int TW_TOTAL = tw_off(NST);
+};
+
+// Registers per thread: 32 complex for fp32, 16 for fp64.
+template <typename Real> struct RmaxOf { static constexpr int v = 32; };
+template <> struct RmaxOf<double> { static constexpr int v = 16; };
+
+// Host-side description of a stage-root table block (for table building).
+struct StageTableInfo {
+  int nst;
+  int radix[8];
+  int ns[8];
+  int total;
+};
+template <int L, int RMAX>
+inline StageTableInfo stage_table_info() {
+  using Sh = Shape<L, RMAX>;
+  StageTableInfo s{};
+  s.nst = Sh::NST;
+  for (int i = 0; i < Sh::NST; ++i) {
+    s.radix[i] = Sh::radix(i);
+    s.ns[i] = Sh::ns(i);
+  }
+  s.total = Sh::TW_TOTAL;
+  return s;
+}
+
+__device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
+
+// ------------------------------------------------------------------ Stockham
+// v[i*RS + q]: input q of butterfly b = t + T*i of the current stage.
+// After the last stage v[i*RS + q] = X[b + q * (L / RS_last)].
+template <typename V, int L, int RMAX, bool INV, int S>
+struct Stages {
+  using Sh = Shape<L, RMAX>;
+  static constexpr int RS = Sh::radix(S), NS = Sh::ns(S), NB = Sh::R / RS;
+  template <class Ex, class Sync>
+  __device__ __forceinline__ static void run(V* v, int t, Ex& ex, const V* __restrict__ tw, Sync& sync) {
+    if constexpr (S > 0) {
+      const V* tws = tw + Sh::tw_off(S);
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const int k = (t + Sh::T * i) & (NS - 1);
+#pragma unroll
+        for (int q = 1; q < RS; ++q) v[i * RS + q] = ctw<INV>(v[i * RS + q], __ldg(tws + q * NS + k));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) reg_dft<RS, INV>(v + i * RS);
+    if constexpr (S + 1 < Sh::NST) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const int b = t + Sh::T * i;
+        const int base = (b / NS) * (NS * RS) + (b & (NS - 1));
+#pragma unroll
+        for (int q = 0; q < RS; ++q) ex(base + q * NS) = v[i * RS + q];
+      }
+      sync();
+      constexpr int RS2 = Sh::radix(S + 1), NB2 = Sh::R / RS2, STR2 = L / RS2;
+#pragma unroll
+      for (int i = 0; i < NB2; ++i) {
+        const int b = t + Sh::T * i;
+#pragma unroll
+        for (int q = 0; q < RS2; ++q) v[i * RS2 + q] = ex(b + q * STR2);
+      }
+      sync();
+      Stages<V, L, RMAX, INV, S + 1>::run(v, t, ex, tw, sync);
+    }
+  }
+};
+
+// output index of register slot j after the last stage
+template <int L, int RMAX>
+__device__ __forceinline__ int out_index(int t, int j) {
+  using Sh = Shape<L, RMAX>;
+  constexpr int RSL = Sh::radix(Sh::NST - 1);
+  const int i = j / RSL, q = j % RSL;
+  return t + Sh::T * i + q * (L / RSL);
+}
+
+struct SyncWarp { __device__ __forceinline__ void operator()() const { __syncwarp(); } };
+struct SyncBlock { __device__ __forceinline__ void operator()() const { __syncthreads(); } };
+
+// Inter-pass root W_M^e, e < M, from coarse/fine tables: W = C[e>>B] * F[e & (2^B-1)].
+template <typename V>
+__device__ __forceinline__ V interpass_root(const V* __restrict__ wc, const V* __restrict__ wf, uint32_t e, int fb) {
+  const V c = __ldg(wc + (e >> fb));
+  const V f = __ldg(wf + (e & ((1u << fb) - 1u)));
+  return cmul(c, f);
+}
+
+// ------------------------------------------------------------------ K_ROWS
+// FPC contiguous length-L rows per CTA, natural order in and out (the p = 1
+// pass of fft_tiled: col_sources bit reversal + dit_levels + identity
+// interleave, tiled_fft.hpp:346-406). In-place safe.
+template <typename Real, int L, int FPC>
+struct RowsCfg {
+  using V = C2<Real>;
+  static constexpr int RMAX = RmaxOf<Real>::v;
+  using Sh = Shape<L, RMAX>;
+  static constexpr int THREADS = FPC * Sh::T;
+  static constexpr int REG = L + L / 32 + 1;  // per-FFT exchange region (elements)
+  static constexpr int SMEM = (Sh::NST > 1 ? FPC * REG : 1) * (int)sizeof(V);
+};
+
+template <typename Real, int L, int FPC, bool INV>
+__global__ void __launch_bounds__(RowsCfg<Real, L, FPC>::THREADS)
+k_rows(const C2<Real>* in, C2<Real>* out, long long nrows, const C2<Real>* __restrict__ tw, Real scale) {
+  using Cfg = RowsCfg<Real, L, FPC>;
+  using V = C2<Real>;
+  using Sh = typename Cfg::Sh;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* sm = reinterpret_cast<V*>(smem_raw);
+  const int ff = threadIdx.x / Sh::T, t = threadIdx.x % Sh::T;
+  long long row = (long long)blockIdx.x * FPC + ff;
+  const bool active = row < nrows;
+  if (!active) row = nrows - 1;
+  const V* src = in + row * L;
+  V v[Sh::R];
+#pragma unroll
+  for (int q = 0; q < Sh::R; ++q) v[q] = src[t + q * Sh::T];
+  V* reg = sm + ff * Cfg::REG;
+  auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
+  if constexpr (Sh::T <= 32) {
+    SyncWarp s;
+    Stages<V, L, Cfg::RMAX, INV, 0>::run(v, t, ex, tw, s);
+  } else {
+    SyncBlock s;
+    Stages<V, L, Cfg::RMAX, INV, 0>::run(v, t, ex, tw, s);
+  }
+  if (active) {
+    V* dst = out + row * L;
+#pragma unroll
+    for (int j = 0; j < Sh::R; ++j) {
+      V r = v[j];
+      if (scale != (Real)1) r = mk(r.x * scale, r.y * scale);
+      dst[out_index<L, Cfg::RMAX>(t, j)] = r;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K_COMB
+// 16 adjacent combs per CTA (lanes along the comb index f, so every
+// global access is 16 contiguous elements = one 128-byte line for fp32).
+//
+// Element n of comb (g, f):   in [ in_base(g) + f + n * s_in ]
+// Spectrum k of comb (g, f):  out[out_base(g) + f + k * s_out] (* W_M^{r k})
+//
+// mode 0 (1D inner pass, tiled_fft.hpp:252-294): tile -> (batch, sub, chunk);
+//   base = batch*bstride + sub*sub_len + chunk*16, s = rows_per_sub,
+//   r = chunk*16 + f, in place.
+// mode 1 (strided transform along an axis with element stride `es`, e.g. the
+//   2D column pass): tile -> (batch, grow, chunk); the 1D pass geometry acts
+//   on the logical index, chunk*16+f selects the column; inner passes are in
+//   place with root r = grow % rows_per_sub, the final pass stores through
+//   the digit interleave (stage_plan.hpp:144-155).
+struct CombArgs {
+  long long bstride;      // elements between batch items
+  long long ntiles;       // total tiles
+  long long chunks;       // f-chunks per group
+  long long groups_per_batch;
+  long long sub_len, rps; // pass geometry (logical units)
+  long long es;           // element stride of the logical index (mode 1)
+  long long out_w_last;   // final pass: out_weights[p-1]
+  int final_pass;         // mode 1 only
+  int fvalid;             // valid lanes per chunk (<= 16)
+  int fb;                 // fine-table bits for W_M
+  uint32_t m_mask;        // M - 1 (M = sub_len)
+  int p;                  // passes of the logical plan (digit interleave)
+  long long out_w[8], sub_w[8];
+};
+
+__device__ __forceinline__ long long final_index_dev(const CombArgs& a, long long sub) {
+  long long out = 0, rem = sub;
+  for (int i = 0; i + 1 < a.p; ++i) {
+    const long long d = rem / a.sub_w[i];
+    rem -= d * a.sub_w[i];
+    out += d * a.out_w[i];
+  }
+  return out;
+}
+
+template <typename Real, int L>
+struct CombCfg {
+  using V = C2<Real>;
+  static constexpr int RMAX = RmaxOf<Real>::v;
+  using Sh = Shape<L, RMAX>;
+  static constexpr int F = 16;
+  static constexpr int THREADS = F * Sh::T;
+  static constexpr int SMEM = (Sh::NST > 1 ? L * F : 1) * (int)sizeof(V);
+};
+
+template <typename Real, int L, bool INV, bool TWID, int MODE>
+__global__ void __launch_bounds__(CombCfg<Real, L>::THREADS)
+k_comb(const C2<Real>* in, C2<Real>* out, CombArgs a, const C2<Real>* __restrict__ tw,
+       const C2<Real>* __restrict__ wc, const C2<Real>* __restrict__ wf, Real scale) {
+  using Cfg = CombCfg<Real, L>;
+  using V = C2<Real>;
+  using Sh = typename Cfg::Sh;
+  constexpr int F = Cfg::F;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* sm = reinterpret_cast<V*>(smem_raw);
+  const int f = threadIdx.x % F, t = threadIdx.x / F;
+  const long long tile = blockIdx.x;
+  const long long chunk = tile % a.chunks;
+  const long long g = tile / a.chunks;
+  const long long batch = g / a.groups_per_batch;
+  const long long u = g % a.groups_per_batch;  // mode 0: sub; mode 1: grow
+  long long in_base, out_base, s_in, s_out;
+  uint32_t r;
+  if constexpr (MODE == 0) {
+    in_base = batch * a.bstride + u * a.sub_len + chunk * F;
+    out_base = in_base;
+    s_in = s_out = a.rps;
+    r = (uint32_t)(chunk * F + f);
+  } else {
+    const long long sub = u / a.rps, rr = u % a.rps;
+    in_base = batch * a.bstride + (sub * a.sub_len + rr) * a.es + chunk * F;
+    s_in = a.rps * a.es;
+    r = (uint32_t)rr;
+    if (a.final_pass) {
+      out_base = batch * a.bstride + final_index_dev(a, u) * a.es + chunk * F;
+      s_out = a.out_w_last * a.es;
+    } else {
+      out_base = in_base;
+      s_out = s_in;
+    }
+  }
+  const bool active = f < a.fvalid;
+  const int fl = active ? f : 0;
+  V v[Sh::R];
+#pragma unroll
+  for (int q = 0; q < Sh::R; ++q) v[q] = in[in_base + fl + (long long)(t + q * Sh::T) * s_in];
+  auto ex = [sm, f](int i) -> V& { return sm[i * F + f]; };
+  SyncBlock s;
+  Stages<V, L, Cfg::RMAX, INV, 0>::run(v, t, ex, tw, s);
+  if (active) {
+#pragma unroll
+    for (int j = 0; j < Sh::R; ++j) {
+      const int k = out_index<L, Cfg::RMAX>(t, j);
+      V x = v[j];
+      if constexpr (TWID) {
+        const uint32_t e = (r * (uint32_t)k) & a.m_mask;
+        const V w = interpass_root(wc, wf, e, a.fb);
+        x = ctw<INV>(x, w);
+      }
+      if (scale != (Real)1) x = mk(x.x * scale, x.y * scale);
+      out[out_base + f + (long long)k * s_out] = x;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K_FINAL_T
+// Final pass of a multi-pass 1D plan (tiled_fft.hpp:295-306): rows are
+// contiguous on input but the digit interleave scatters each spectrum with
+// stride out_weights[p-1]. The CTA takes the 16 rows whose leading digit d0
+// is consecutive (grow = d0*sub_w[0] + o), so for every k the 16 results are
+// 16 consecutive outputs; the row FFTs run lanes-along-n (coalesced loads),
+// then one padded [k][17] shared-memory transpose turns the lanes around for
+// 128-byte stores.
+struct FinalArgs {
+  long long bstride, n;      // batch stride, transform length
+  long long ntiles, chunks;  // chunks = f0 / 16
+  long long sw0;             // sub_weights[0]
+  long long out_w_last;
+  int p;
+  long long out_w[8], sub_w[8];
+};
+
+template <typename Real, int L>
+struct FinalCfg {
+  using V = C2<Real>;
+  static constexpr int RMAX = RmaxOf<Real>::v;
+  using Sh = Shape<L, RMAX>;
+  static constexpr int F = 16;
+  static constexpr int THREADS = F * Sh::T;
+  static constexpr int REG = L + L / 32 + 1;
+  static constexpr int A = F * REG, B = L * (F + 1);
+  static constexpr int SMEM = (A > B ? A : B) * (int)sizeof(V);
+};
+
+template <typename Real, int L, bool INV>
+__global__ void __launch_bounds__(FinalCfg<Real, L>::THREADS)
+k_final_t(const C2<Real>* in, C2<Real>* out, FinalArgs a, const C2<Real>* __restrict__ tw, Real scale) {
+  using Cfg = FinalCfg<Real, L>;
+  using V = C2<Real>;
+  using Sh = typename Cfg::Sh;
+  constexpr int F = Cfg::F;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* sm = reinterpret_cast<V*>(smem_raw);
+  const long long tile = blockIdx.x;
+  const long long per_batch = a.ntiles / 1;  // tiles already include batch
+  (void)per_batch;
+  const long long tiles_per_batch = a.chunks * a.sw0;
+  const long long batch = tile / tiles_per_batch;
+  const long long rem = tile % tiles_per_batch;
+  const long long o = rem % a.sw0, chunk = rem / a.sw0;
+  // phase 1: FFT of row (chunk*16 + ff)*sw0 + o, lanes along n
+  {
+    const int ff = threadIdx.x / Sh::T, t = threadIdx.x % Sh::T;
+    const long long grow = (chunk * F + ff) * a.sw0 + o;
+    const V* src = in + batch * a.bstride + grow * L;
+    V v[Sh::R];
+#pragma unroll
+    for (int q = 0; q < Sh::R; ++q) v[q] = src[t + q * Sh::T];
+    V* reg = sm + ff * Cfg::REG;
+    auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
+    SyncBlock s;
+    Stages<V, L, Cfg::RMAX, INV, 0>::run(v, t, ex, tw, s);
+    __syncthreads();  // exchange regions are reused by the transpose below
+#pragma unroll
+    for (int j = 0; j < Sh::R; ++j) sm[out_index<L, Cfg::RMAX>(t, j) * (F + 1) + ff] = v[j];
+  }
+  __syncthreads();
+  // phase 2: lanes along the 16 consecutive outputs
+  {
+    const int f = threadIdx.x % F, kk = threadIdx.x / F;
+    constexpr int KSTEP = Cfg::THREADS / F;
+    // out index of (d0 = chunk*16 + f, other digits from o) = d0 + final(o)
+    const long long ob = batch * a.bstride + chunk * F + f + [&] {
+      long long outi = 0, r2 = o;
+      for (int i = 0; i + 1 < a.p; ++i) {
+        const long long d = r2 / a.sub_w[i];
+        r2 -= d * a.sub_w[i];
+        outi += d * a.out_w[i];
+      }
+      return outi;
+    }();
+#pragma unroll 4
+    for (int k = kk; k < L; k += KSTEP) {
+      V x = sm[k * (F + 1) + f];
+      if (scale != (Real)1) x = mk(x.x * scale, x.y * scale);
+      out[ob + (long long)k * a.out_w_last] = x;
+    }
+  }
+}
+
+}  // namespace tfb

@@ -1,0 +1,783 @@
+// tilefft_b200: plan objects, pass scheduling and the C ABI
+// (include/tilefft_b200.h). Host side of the B200 path: it owns the device
+// twiddle tables (the paper's precomputed "texture" roots),
+// the ping-pong workspace (tiled_fft.hpp:338-344) and the launch sequence of
+// one fft_tiled call (tiled_fft.hpp:346-405), one kernel per pass.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include "../../include/tilefft_b200.h"
+#include "exact_kernels.cuh"
+#include "fast_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess) return fail(TILEFFT_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+bool is_pow2(uint64_t v) { return v != 0 && (v & (v - 1)) == 0; }
+int ilog2(uint64_t v) { return 63 - __builtin_clzll(v); }
+
+// ---------------------------------------------------------------- roots
+// exp(-2 pi i j / m) with the reference's construction (twiddle.hpp:47-73):
+// double angle, cos/sin cast to Real, quadrant mirroring, exact axis points.
+// Values are resolution independent (scaling j and m by a power of two gives
+// the same double angle), so any W_m^j equals the reference table's entry.
+template <typename Real>
+void ref_root(uint64_t j, uint64_t m, Real* re, Real* im) {
+  j &= (m - 1);
+  if (j == 0) { *re = 1; *im = 0; return; }
+  if (2 * j == m) { *re = -1; *im = 0; return; }
+  if (m >= 4 && 4 * j == m) { *re = 0; *im = -1; return; }
+  if (m >= 4 && 4 * j == 3 * m) { *re = 0; *im = 1; return; }
+  const uint64_t q = m / 4;
+  // first quadrant index and mirror (twiddle.hpp:63-70)
+  uint64_t jj;
+  int sc, ss;  // signs applied to (c, s) -> value = (sc*c, ss*s)
+  if (j < q) { jj = j; sc = 1; ss = -1; }
+  else if (j < 2 * q) { jj = m / 2 - j; sc = -1; ss = -1; }
+  else if (j < 3 * q) { jj = j - m / 2; sc = -1; ss = 1; }
+  else { jj = m - j; sc = 1; ss = 1; }
+  const double angle = 2.0 * 3.141592653589793238462643383279502884 * (double)jj / (double)m;
+  const Real c = (Real)std::cos(angle), s = (Real)std::sin(angle);
+  *re = sc > 0 ? c : -c;
+  *im = ss > 0 ? s : -s;
+}
+
+// Accurate fp64 root for fast-mode tables (rounded once to Real).
+template <typename Real>
+void acc_root(uint64_t j, uint64_t m, Real* re, Real* im) { ref_root<Real>(j, m, re, im); }
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() { if (p) cudaFree(p); }
+  int alloc(size_t b) {
+    if (b == 0) return 0;
+    if (cudaMalloc(&p, b) != cudaSuccess) { cudaGetLastError(); p = nullptr; return fail(TILEFFT_ENOMEM, "cudaMalloc(%zu) failed", b); }
+    bytes = b;
+    return 0;
+  }
+};
+
+enum PassKind { K_ROWS = 0, K_COMB1D = 1, K_COMBAX = 2, K_FINALT = 3, K_EXACT = 4 };
+
+struct Pass {
+  PassKind kind;
+  int L;
+  int src, dst;              // 0 = user input, 1 = user output, 2 = workspace
+  long long grid;
+  size_t smem;
+  tfb::CombArgs comb;
+  tfb::FinalArgs fin;
+  tfb::ExactArgs ex;
+  long long nrows;           // K_ROWS
+  size_t tw_off;             // offset (elements) of this L's Stockham table in the table buffer
+  size_t wc_off, wf_off;     // inter-pass tables
+  bool twid;
+  bool final_pass;           // the pass that applies the inverse scale
+};
+
+}  // namespace
+
+struct tilefft_plan_s {
+  int device = 0;
+  uint64_t n = 0, batch = 0, ny = 0, nx = 0;
+  uint32_t elem_bytes = 8, mode = 0, is2d = 0;
+  std::vector<uint64_t> dev_factors;
+  std::vector<Pass> passes;
+  DevBuf tables;          // all device tables (elements of C2<Real>)
+  DevBuf work;            // workspace (batch * n elements)
+  size_t table_elems = 0;
+  // host-path staging
+  std::mutex host_mu;
+  cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t hev[3] = {nullptr, nullptr, nullptr};
+  DevBuf hbuf[3];
+  uint64_t host_chunk = 0;  // transforms per pipelined chunk
+  ~tilefft_plan_s() {
+    for (int i = 0; i < 3; ++i) {
+      if (hs[i]) cudaStreamDestroy(hs[i]);
+      if (hev[i]) cudaEventDestroy(hev[i]);
+    }
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------- table builder
+template <typename Real>
+struct TableBuilder {
+  std::vector<Real> h;  // interleaved
+  size_t add(size_t count) {
+    size_t off = h.size() / 2;
+    h.resize(h.size() + 2 * count);
+    return off;
+  }
+  void set(size_t idx, Real re, Real im) { h[2 * idx] = re; h[2 * idx + 1] = im; }
+};
+
+template <typename Real>
+tfb::StageTableInfo stage_info_for(int L) {
+  constexpr int RM = tfb::RmaxOf<Real>::v;
+  switch (L) {
+#define CASE(LL) case LL: return tfb::stage_table_info<LL, RM>();
+    CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64) CASE(128) CASE(256) CASE(512) CASE(1024)
+    CASE(2048) CASE(4096) CASE(8192)
+#undef CASE
+  }
+  return tfb::StageTableInfo{};
+}
+
+// Stockham stage roots for length L: block of [q][k] tables, stage s >= 1,
+// entry q*Ns + k = W_{Ns*Rs}^{q k}.
+template <typename Real>
+size_t add_stage_table(TableBuilder<Real>& tb, int L) {
+  const tfb::StageTableInfo si = stage_info_for<Real>(L);
+  const size_t off = tb.add(std::max(si.total, 1));
+  size_t pos = off;
+  for (int s = 1; s < si.nst; ++s) {
+    const uint64_t rs = si.radix[s], ns = si.ns[s], m = rs * ns;
+    for (uint64_t q = 0; q < rs; ++q)
+      for (uint64_t k = 0; k < ns; ++k) {
+        Real re, im;
+        acc_root<Real>(q * k, m, &re, &im);
+        tb.set(pos++, re, im);
+      }
+  }
+  return off;
+}
+
+// Inter-pass roots W_M^e = C[e >> fb] * F[e & (2^fb - 1)].
+template <typename Real>
+void add_interpass(TableBuilder<Real>& tb, uint64_t M, size_t* wc, size_t* wf, int* fb) {
+  const int lm = ilog2(M);
+  *fb = (lm + 1) / 2;
+  const uint64_t nf = 1ull << *fb, nc = M >> *fb;
+  *wc = tb.add(nc);
+  for (uint64_t i = 0; i < nc; ++i) {
+    Real re, im;
+    acc_root<Real>(i * nf, M, &re, &im);
+    tb.set(*wc + i, re, im);
+  }
+  *wf = tb.add(nf);
+  for (uint64_t j = 0; j < nf; ++j) {
+    Real re, im;
+    acc_root<Real>(j, M, &re, &im);
+    tb.set(*wf + j, re, im);
+  }
+}
+
+// make_plan's factorisation (stage_plan.hpp:82-95) and weights (:116-125).
+struct Geo {
+  std::vector<uint64_t> f, sub_len, rps, out_w, sub_w;
+};
+Geo geometry(uint64_t n, const std::vector<uint64_t>& f) {
+  Geo g;
+  g.f = f;
+  const size_t p = f.size();
+  uint64_t sl = n;
+  for (size_t s = 0; s < p; ++s) {
+    g.sub_len.push_back(sl);
+    g.rps.push_back(sl / f[s]);
+    sl /= f[s];
+  }
+  g.out_w.assign(p, 1);
+  for (size_t i = 1; i < p; ++i) g.out_w[i] = g.out_w[i - 1] * f[i - 1];
+  g.sub_w.assign(p > 1 ? p - 1 : 0, 1);
+  for (size_t i = p - 1; i-- > 0;) g.sub_w[i] = (i + 1 < p - 1) ? g.sub_w[i + 1] * f[i + 1] : 1;
+  return g;
+}
+std::vector<uint64_t> balanced_factors(uint64_t n, uint64_t cap) {
+  const int b = ilog2(n), c = ilog2(cap);
+  const int p = (b + c - 1) / c, base = b / p, extra = b % p;
+  std::vector<uint64_t> f;
+  for (int s = 0; s < p; ++s) f.push_back(1ull << (base + (s < extra ? 1 : 0)));
+  return f;
+}
+
+// ---------------------------------------------------------------- kernel dispatch
+// Opt a kernel into >48 KB dynamic shared memory once per (function, device).
+std::mutex g_attr_mu;
+struct AttrRec { const void* fn; int dev; int bytes; };
+std::vector<AttrRec> g_attr_done;
+int ensure_smem(const void* fn, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  for (auto& r : g_attr_done)
+    if (r.fn == fn && r.dev == dev) {
+      if (r.bytes >= bytes) return 0;
+      CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      r.bytes = bytes;
+      return 0;
+    }
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  g_attr_done.push_back({fn, dev, bytes});
+  return 0;
+}
+
+// FFTs per CTA for K_ROWS: 8 warps of work for L <= 1024 (fp32), one FFT per CTA above.
+template <typename Real>
+constexpr int rows_fpc(int L) {
+  constexpr int RM = tfb::RmaxOf<Real>::v;
+  if (L >= 2048) return 1;
+  const int T = L < RM ? 1 : L / RM;
+  const int f = 256 / T;
+  return f < 1 ? 1 : f;
+}
+
+template <typename Real, int L, bool INV>
+int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, Real scale, cudaStream_t st) {
+  constexpr int FPC = rows_fpc<Real>(L);
+  using Cfg = tfb::RowsCfg<Real, L, FPC>;
+  auto k = tfb::k_rows<Real, L, FPC, INV>;
+  if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
+  const long long grid = (ps.nrows + FPC - 1) / FPC;
+  k<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, st>>>((const tfb::C2<Real>*)in, (tfb::C2<Real>*)out, ps.nrows,
+                                                     (const tfb::C2<Real>*)tw + ps.tw_off, scale);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <typename Real, int L, bool INV>
+int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, Real scale, cudaStream_t st) {
+  using Cfg = tfb::CombCfg<Real, L>;
+  using V = tfb::C2<Real>;
+  const V* t = (const V*)tb;
+  auto go = [&](auto k) -> int {
+    if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
+    k<<<(unsigned)ps.grid, Cfg::THREADS, Cfg::SMEM, st>>>((const V*)in, (V*)out, ps.comb, t + ps.tw_off,
+                                                          t + ps.wc_off, t + ps.wf_off, scale);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  };
+  if (ps.kind == K_COMB1D) return go(tfb::k_comb<Real, L, INV, true, 0>);
+  if (ps.twid) return go(tfb::k_comb<Real, L, INV, true, 1>);
+  return go(tfb::k_comb<Real, L, INV, false, 1>);
+}
+
+template <typename Real, int L, bool INV>
+int launch_final(const Pass& ps, const void* in, void* out, const void* tb, Real scale, cudaStream_t st) {
+  using Cfg = tfb::FinalCfg<Real, L>;
+  using V = tfb::C2<Real>;
+  auto k = tfb::k_final_t<Real, L, INV>;
+  if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
+  k<<<(unsigned)ps.grid, Cfg::THREADS, Cfg::SMEM, st>>>((const V*)in, (V*)out, ps.fin, (const V*)tb + ps.tw_off,
+                                                        scale);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <typename Real, bool INV>
+int launch_fast(const Pass& ps, const void* in, void* out, const void* tb, Real scale, cudaStream_t st) {
+#define DISPATCH(FN, ...)                                                     \
+  switch (ps.L) {                                                             \
+    case 2: return FN<Real, 2, INV>(ps, in, out, tb, scale, st);              \
+    case 4: return FN<Real, 4, INV>(ps, in, out, tb, scale, st);              \
+    case 8: return FN<Real, 8, INV>(ps, in, out, tb, scale, st);              \
+    case 16: return FN<Real, 16, INV>(ps, in, out, tb, scale, st);            \
+    case 32: return FN<Real, 32, INV>(ps, in, out, tb, scale, st);            \
+    case 64: return FN<Real, 64, INV>(ps, in, out, tb, scale, st);            \
+    case 128: return FN<Real, 128, INV>(ps, in, out, tb, scale, st);          \
+    case 256: return FN<Real, 256, INV>(ps, in, out, tb, scale, st);          \
+    case 512: return FN<Real, 512, INV>(ps, in, out, tb, scale, st);          \
+    case 1024: return FN<Real, 1024, INV>(ps, in, out, tb, scale, st);        \
+    __VA_ARGS__                                                               \
+  }
+  if (ps.kind == K_ROWS) {
+    DISPATCH(launch_rows,
+             case 2048: return launch_rows<Real, 2048, INV>(ps, in, out, tb, scale, st);
+             case 4096: return launch_rows<Real, 4096, INV>(ps, in, out, tb, scale, st);
+             case 8192: return launch_rows<Real, 8192, INV>(ps, in, out, tb, scale, st);)
+  } else if (ps.kind == K_COMB1D || ps.kind == K_COMBAX) {
+    DISPATCH(launch_comb)
+  } else if (ps.kind == K_FINALT) {
+    DISPATCH(launch_final)
+  }
+#undef DISPATCH
+  return fail(TILEFFT_EINVAL, "internal: no kernel for pass length %d", ps.L);
+}
+
+template <typename Real>
+int launch_exact(const Pass& ps, const void* in, void* out, const void* tb, Real scale, int conj_in, int conj_out,
+                 cudaStream_t st) {
+  using V = tfb::C2<Real>;
+  tfb::ExactArgs a = ps.ex;
+  a.conj_in = conj_in;
+  a.conj_scale_out = conj_out;
+  auto k = tfb::k_exact_pass<Real>;
+  const size_t smem = (size_t)a.L * sizeof(V);
+  if (int rc = ensure_smem((const void*)k, (int)smem)) return rc;
+  int threads = (int)std::min<long long>(256, std::max<long long>(32, a.L / 2));
+  k<<<(unsigned)ps.grid, threads, smem, st>>>((const V*)in, (V*)out, a, (const V*)tb, scale);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------- plan building
+template <typename Real>
+int build_fast_1d(tilefft_plan_s* P, TableBuilder<Real>& tb) {
+  const uint64_t n = P->n, B = P->batch;
+  if (n <= 8192) {
+    Pass ps{};
+    ps.kind = K_ROWS;
+    ps.L = (int)n;
+    ps.src = 0;
+    ps.dst = 1;
+    ps.nrows = (long long)B;
+    ps.tw_off = add_stage_table(tb, (int)n);
+    ps.final_pass = true;
+    P->passes.push_back(ps);
+    P->dev_factors = {n};
+    return 0;
+  }
+  const std::vector<uint64_t> f = balanced_factors(n, 1024);
+  const Geo g = geometry(n, f);
+  const size_t p = f.size();
+  if (p > 8) return fail(TILEFFT_EINVAL, "transform too long for the fast path (%zu passes)", p);
+  for (size_t s = 0; s < p; ++s) {
+    Pass ps{};
+    ps.L = (int)f[s];
+    ps.tw_off = add_stage_table(tb, ps.L);
+    if (s + 1 < p) {
+      ps.kind = K_COMB1D;
+      ps.src = s == 0 ? 0 : 2;
+      ps.dst = 2;
+      ps.twid = true;
+      int fb;
+      add_interpass(tb, g.sub_len[s], &ps.wc_off, &ps.wf_off, &fb);
+      tfb::CombArgs& a = ps.comb;
+      a.bstride = (long long)n;
+      a.chunks = (long long)(g.rps[s] / 16);
+      a.groups_per_batch = (long long)(n / g.sub_len[s]);
+      a.ntiles = a.chunks * a.groups_per_batch * (long long)B;
+      a.sub_len = (long long)g.sub_len[s];
+      a.rps = (long long)g.rps[s];
+      a.es = 1;
+      a.fvalid = 16;
+      a.fb = fb;
+      a.m_mask = (uint32_t)(g.sub_len[s] - 1);
+      a.p = (int)p;
+      ps.grid = a.ntiles;
+    } else {
+      ps.kind = K_FINALT;
+      ps.src = p == 1 ? 0 : 2;
+      ps.dst = 1;
+      ps.final_pass = true;
+      tfb::FinalArgs& a = ps.fin;
+      a.bstride = (long long)n;
+      a.n = (long long)n;
+      a.sw0 = (long long)g.sub_w[0];
+      a.chunks = (long long)(f[0] / 16);
+      a.ntiles = a.chunks * a.sw0 * (long long)B;
+      a.out_w_last = (long long)g.out_w[p - 1];
+      a.p = (int)p;
+      for (size_t i = 0; i < p; ++i) a.out_w[i] = (long long)g.out_w[i];
+      for (size_t i = 0; i + 1 < p; ++i) a.sub_w[i] = (long long)g.sub_w[i];
+      ps.grid = a.ntiles;
+    }
+    P->passes.push_back(ps);
+  }
+  P->dev_factors = f;
+  return 0;
+}
+
+// Column (strided-axis) passes of a 2D transform: logical length ny, element
+// stride nx, nx columns, `B` images. Inner passes in place on `buf`; the final
+// pass writes `dst`.
+template <typename Real>
+int build_axis_passes(tilefft_plan_s* P, TableBuilder<Real>& tb, uint64_t ny, uint64_t nx, uint64_t B, int buf,
+                      int dst) {
+  const std::vector<uint64_t> f = ny <= 1024 ? std::vector<uint64_t>{ny} : balanced_factors(ny, 1024);
+  const Geo g = geometry(ny, f);
+  const size_t p = f.size();
+  for (size_t s = 0; s < p; ++s) {
+    Pass ps{};
+    ps.kind = K_COMBAX;
+    ps.L = (int)f[s];
+    ps.tw_off = add_stage_table(tb, ps.L);
+    ps.src = buf;
+    ps.dst = (s + 1 == p) ? dst : buf;
+    ps.twid = s + 1 < p;
+    ps.final_pass = s + 1 == p;
+    tfb::CombArgs& a = ps.comb;
+    int fb = 0;
+    if (ps.twid) add_interpass(tb, g.sub_len[s], &ps.wc_off, &ps.wf_off, &fb);
+    a.bstride = (long long)(ny * nx);
+    a.chunks = (long long)((nx + 15) / 16);
+    a.fvalid = (int)std::min<uint64_t>(16, nx);
+    a.groups_per_batch = (long long)(ny / f[s]);  // rows of this pass
+    a.ntiles = a.chunks * a.groups_per_batch * (long long)B;
+    a.sub_len = (long long)g.sub_len[s];
+    a.rps = (long long)g.rps[s];
+    a.es = (long long)nx;
+    a.final_pass = ps.final_pass ? 1 : 0;
+    a.out_w_last = (long long)g.out_w[p - 1];
+    a.fb = fb;
+    a.m_mask = (uint32_t)(g.sub_len[s] - 1);
+    a.p = (int)p;
+    for (size_t i = 0; i < p; ++i) a.out_w[i] = (long long)g.out_w[i];
+    for (size_t i = 0; i + 1 < p; ++i) a.sub_w[i] = (long long)g.sub_w[i];
+    ps.grid = a.ntiles;
+    P->passes.push_back(ps);
+    P->dev_factors.push_back(f[s]);
+  }
+  return 0;
+}
+
+template <typename Real>
+int build_exact(tilefft_plan_s* P, TableBuilder<Real>& tb, const std::vector<uint64_t>& f, const void* tv,
+                uint64_t tres) {
+  const uint64_t n = P->n;
+  const Geo g = geometry(n, f);
+  const size_t p = f.size();
+  if (p > 64) return fail(TILEFFT_EINVAL, "fft_tiled: empty plan");
+  for (uint64_t L : f)
+    if (L * sizeof(tfb::C2<Real>) > 227 * 1024)
+      return fail(TILEFFT_EINVAL, "exact mode: pass length %llu exceeds one CTA's shared memory",
+                  (unsigned long long)L);
+  // exact roots: W_n^e for e < n, straight from the caller's table when given
+  if (P->mode == TILEFFT_MODE_EXACT) {
+    const size_t off = tb.add(n);
+    if (tv != nullptr) {
+      const Real* v = (const Real*)tv;
+      const uint64_t stride = tres / n;
+      for (uint64_t e = 0; e < n; ++e) tb.set(off + e, v[2 * e * stride], v[2 * e * stride + 1]);
+    } else {
+      for (uint64_t e = 0; e < n; ++e) {
+        Real re, im;
+        ref_root<Real>(e, n, &re, &im);
+        tb.set(off + e, re, im);
+      }
+    }
+  }
+  for (size_t s = 0; s < p; ++s) {
+    Pass ps{};
+    ps.kind = K_EXACT;
+    ps.L = (int)f[s];
+    ps.src = s == 0 ? 0 : 2;
+    ps.dst = (s + 1 == p) ? 1 : 2;
+    ps.final_pass = s + 1 == p;
+    tfb::ExactArgs& a = ps.ex;
+    a.n = (long long)n;
+    a.rows = (long long)(n / f[s]);
+    a.bstride = (long long)n;
+    a.L = (long long)f[s];
+    a.sub_len = (long long)g.sub_len[s];
+    a.rps = (long long)g.rps[s];
+    a.levels = ilog2(f[s]);
+    a.has_inter = s + 1 < p;
+    a.p = (int)p;
+    a.permute_only = P->mode == TILEFFT_MODE_PERMUTE;
+    for (size_t i = 0; i < p; ++i) a.out_w[i] = (long long)g.out_w[i];
+    for (size_t i = 0; i + 1 < p; ++i) a.sub_w[i] = (long long)g.sub_w[i];
+    ps.grid = a.rows * (long long)P->batch;
+    P->passes.push_back(ps);
+  }
+  P->dev_factors = f;
+  return 0;
+}
+
+int check_device(int device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(TILEFFT_ENODEV, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  if (device < 0 || device >= count) return fail(TILEFFT_ENODEV, "device %d out of range (%d devices)", device, count);
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(TILEFFT_ENODEV, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
+  CUDA_TRY(cudaSetDevice(device));
+  return 0;
+}
+
+template <typename Real>
+int finish_plan(tilefft_plan_s* P, TableBuilder<Real>& tb) {
+  // workspace when any pass touches it
+  bool need_work = false;
+  for (const Pass& ps : P->passes) need_work |= (ps.src == 2 || ps.dst == 2);
+  const uint64_t elems = P->is2d ? P->ny * P->nx * P->batch : P->n * P->batch;
+  if (need_work) {
+    int rc = P->work.alloc(elems * sizeof(tfb::C2<Real>));
+    if (rc) return rc;
+  }
+  P->table_elems = tb.h.size() / 2;
+  if (P->table_elems) {
+    int rc = P->tables.alloc(tb.h.size() * sizeof(Real));
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpy(P->tables.p, tb.h.data(), tb.h.size() * sizeof(Real), cudaMemcpyHostToDevice));
+  }
+  return 0;
+}
+
+template <typename Real>
+int exec_impl(tilefft_plan_s* P, const void* in, void* out, int sign, cudaStream_t st) {
+  const bool inv = sign == TILEFFT_INVERSE;
+  const uint64_t total = P->is2d ? P->ny * P->nx : P->n;
+  const Real scale = inv ? (Real)1 / (Real)total : (Real)1;
+  auto buf = [&](int id) -> void* { return id == 0 ? const_cast<void*>(in) : id == 1 ? out : P->work.p; };
+  for (const Pass& ps : P->passes) {
+    int rc;
+    const void* src = buf(ps.src);
+    void* dst = buf(ps.dst);
+    if (ps.kind == K_EXACT) {
+      const bool first = &ps == &P->passes.front();
+      rc = launch_exact<Real>(ps, src, dst, P->tables.p, scale, inv && first, inv && ps.final_pass, st);
+    } else if (inv) {
+      rc = launch_fast<Real, true>(ps, src, dst, P->tables.p, ps.final_pass ? scale : (Real)1, st);
+    } else {
+      rc = launch_fast<Real, false>(ps, src, dst, P->tables.p, (Real)1, st);
+    }
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+const char* tilefft_last_error(void) { return g_err.c_str(); }
+const char* tilefft_version(void) { return "tilefft_b200 0.1 sm_100a"; }
+
+int tilefft_build_twiddle(uint64_t resolution, uint32_t elem_bytes, void* out) {
+  g_err.clear();
+  if (!is_pow2(resolution) || resolution < 2)
+    return fail(TILEFFT_EINVAL, "build_twiddle_table: resolution must be a power of two >= 2");
+  if (elem_bytes != 8 && elem_bytes != 16) return fail(TILEFFT_EINVAL, "build_twiddle_table: elem_bytes must be 8 or 16");
+  if (!out) return fail(TILEFFT_EINVAL, "build_twiddle_table: null output");
+  for (uint64_t j = 0; j < resolution; ++j) {
+    if (elem_bytes == 8) {
+      float* o = (float*)out;
+      ref_root<float>(j, resolution, &o[2 * j], &o[2 * j + 1]);
+    } else {
+      double* o = (double*)out;
+      ref_root<double>(j, resolution, &o[2 * j], &o[2 * j + 1]);
+    }
+  }
+  return 0;
+}
+
+int tilefft_plan_create(tilefft_plan_t* out, uint64_t n, uint64_t batch, const uint64_t* factors, uint32_t nfactors,
+                        uint32_t elem_bytes, uint32_t mode, const void* tv, uint64_t tres, int device) {
+  g_err.clear();
+  if (!out) return fail(TILEFFT_EINVAL, "tilefft_plan_create: null plan pointer");
+  *out = nullptr;
+  if (!is_pow2(n) || n < 2) return fail(TILEFFT_EINVAL, "make_plan: n must be a power of two >= 2");
+  if (batch < 1) return fail(TILEFFT_EINVAL, "tilefft_plan_create: batch must be >= 1");
+  if (elem_bytes != 8 && elem_bytes != 16) return fail(TILEFFT_EINVAL, "tilefft_plan_create: elem_bytes must be 8 or 16");
+  if (mode > TILEFFT_MODE_PERMUTE) return fail(TILEFFT_EINVAL, "tilefft_plan_create: unknown mode %u", mode);
+  std::vector<uint64_t> f;
+  if (factors && nfactors) {
+    uint64_t prod = 1;
+    for (uint32_t i = 0; i < nfactors; ++i) {
+      if (!is_pow2(factors[i]) || factors[i] < 2) return fail(TILEFFT_EINVAL, "plan factors must be powers of two >= 2");
+      prod *= factors[i];
+      f.push_back(factors[i]);
+    }
+    if (prod != n) return fail(TILEFFT_EINVAL, "fft_tiled: signal length does not match the plan");
+  }
+  if (mode != TILEFFT_MODE_FAST && f.empty()) return fail(TILEFFT_EINVAL, "fft_tiled: empty plan");
+  if (mode == TILEFFT_MODE_EXACT && tv != nullptr &&
+      !(tres >= n && is_pow2(tres) && tres % n == 0))
+    return fail(TILEFFT_EINVAL, "fft_tiled: signal length must divide the table resolution");
+  if (int rc = check_device(device)) return rc;
+  tilefft_plan_s* P = new (std::nothrow) tilefft_plan_s();
+  if (!P) return fail(TILEFFT_ENOMEM, "out of host memory");
+  P->device = device;
+  P->n = n;
+  P->batch = batch;
+  P->elem_bytes = elem_bytes;
+  P->mode = mode;
+  int rc;
+  if (elem_bytes == 8) {
+    TableBuilder<float> tb;
+    rc = mode == TILEFFT_MODE_FAST ? build_fast_1d<float>(P, tb) : build_exact<float>(P, tb, f, tv, tres);
+    if (!rc) rc = finish_plan<float>(P, tb);
+  } else {
+    TableBuilder<double> tb;
+    rc = mode == TILEFFT_MODE_FAST ? build_fast_1d<double>(P, tb) : build_exact<double>(P, tb, f, tv, tres);
+    if (!rc) rc = finish_plan<double>(P, tb);
+  }
+  if (rc) {
+    delete P;
+    return rc;
+  }
+  *out = P;
+  return 0;
+}
+
+int tilefft_plan_create_2d(tilefft_plan_t* out, uint64_t ny, uint64_t nx, uint64_t batch, uint32_t elem_bytes,
+                           int device) {
+  g_err.clear();
+  if (!out) return fail(TILEFFT_EINVAL, "tilefft_plan_create_2d: null plan pointer");
+  *out = nullptr;
+  if (!is_pow2(ny) || !is_pow2(nx) || ny < 2 || nx < 2)
+    return fail(TILEFFT_EINVAL, "make_plan: n must be a power of two >= 2");
+  if (batch < 1) return fail(TILEFFT_EINVAL, "tilefft_plan_create_2d: batch must be >= 1");
+  if (elem_bytes != 8 && elem_bytes != 16) return fail(TILEFFT_EINVAL, "tilefft_plan_create_2d: elem_bytes must be 8 or 16");
+  if (nx > 8192) return fail(TILEFFT_EINVAL, "tilefft_plan_create_2d: rows longer than 8192 are not supported yet");
+  if (int rc = check_device(device)) return rc;
+  tilefft_plan_s* P = new (std::nothrow) tilefft_plan_s();
+  if (!P) return fail(TILEFFT_ENOMEM, "out of host memory");
+  P->device = device;
+  P->is2d = 1;
+  P->ny = ny;
+  P->nx = nx;
+  P->n = ny * nx;
+  P->batch = batch;
+  P->elem_bytes = elem_bytes;
+  P->mode = TILEFFT_MODE_FAST;
+  auto build = [&](auto tbv) -> int {
+    using Real = std::remove_reference_t<decltype(tbv.h[0])>;
+    TableBuilder<Real> tb;
+    const bool multi = ny > 1024;
+    Pass rows{};
+    rows.kind = K_ROWS;
+    rows.L = (int)nx;
+    rows.src = 0;
+    rows.dst = multi ? 2 : 1;
+    rows.nrows = (long long)(ny * batch);
+    rows.tw_off = add_stage_table(tb, (int)nx);
+    P->passes.push_back(rows);
+    P->dev_factors.push_back(nx);
+    int rc = build_axis_passes<Real>(P, tb, ny, nx, batch, multi ? 2 : 1, 1);
+    if (rc) return rc;
+    return finish_plan<Real>(P, tb);
+  };
+  int rc = elem_bytes == 8 ? build(TableBuilder<float>{}) : build(TableBuilder<double>{});
+  if (rc) {
+    delete P;
+    return rc;
+  }
+  *out = P;
+  return 0;
+}
+
+int tilefft_exec_c2c(tilefft_plan_t P, const void* in, void* out, int sign, void* stream) {
+  g_err.clear();
+  if (!P) return fail(TILEFFT_EINVAL, "tilefft_exec_c2c: null plan");
+  if (!in || !out) return fail(TILEFFT_EINVAL, "tilefft_exec_c2c: null buffer");
+  if (sign != TILEFFT_FORWARD && sign != TILEFFT_INVERSE) return fail(TILEFFT_EINVAL, "tilefft_exec_c2c: sign must be -1 or +1");
+  if (P->mode == TILEFFT_MODE_PERMUTE && sign != TILEFFT_FORWARD)
+    return fail(TILEFFT_EINVAL, "tilefft_exec_c2c: permute mode is forward only");
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  return P->elem_bytes == 8 ? exec_impl<float>(P, in, out, sign, st) : exec_impl<double>(P, in, out, sign, st);
+}
+
+int tilefft_exec_c2c_host(tilefft_plan_t P, const void* h_in, void* h_out, int sign) {
+  g_err.clear();
+  if (!P) return fail(TILEFFT_EINVAL, "tilefft_exec_c2c_host: null plan");
+  if (!h_in || !h_out) return fail(TILEFFT_EINVAL, "tilefft_exec_c2c_host: null buffer");
+  std::lock_guard<std::mutex> lock(P->host_mu);
+  CUDA_TRY(cudaSetDevice(P->device));
+  const uint64_t per = P->n;  // elements per transform (2D: ny*nx)
+  const size_t eb = P->elem_bytes;
+  const uint64_t B = P->batch;
+  // chunked pipeline only for single-pass batched plans whose passes act per transform
+  const bool chunkable = B > 1 && P->passes.size() == 1 && P->passes[0].kind != K_EXACT && !P->is2d;
+  if (!chunkable) {
+    const size_t bytes = per * B * eb;
+    if (!P->hbuf[0].p) {
+      if (int rc = P->hbuf[0].alloc(bytes)) return rc;
+    }
+    CUDA_TRY(cudaMemcpy(P->hbuf[0].p, h_in, bytes, cudaMemcpyHostToDevice));
+    if (int rc = tilefft_exec_c2c(P, P->hbuf[0].p, P->hbuf[0].p, sign, nullptr)) return rc;
+    CUDA_TRY(cudaMemcpy(h_out, P->hbuf[0].p, bytes, cudaMemcpyDeviceToHost));
+    return 0;
+  }
+  // ~32 MiB chunks over 3 streams: H2D(i+1) || kernel(i) || D2H(i-1)
+  if (!P->host_chunk) {
+    uint64_t c = std::max<uint64_t>(1, (32ull << 20) / (per * eb));
+    P->host_chunk = std::min<uint64_t>(c, B);
+    for (int i = 0; i < 3; ++i) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&P->hs[i], cudaStreamNonBlocking));
+      if (int rc = P->hbuf[i].alloc(P->host_chunk * per * eb)) return rc;
+    }
+  }
+  const uint64_t C = P->host_chunk;
+  Pass ps = P->passes[0];
+  int ci = 0;
+  for (uint64_t b0 = 0; b0 < B; b0 += C, ci = (ci + 1) % 3) {
+    const uint64_t nb = std::min<uint64_t>(C, B - b0);
+    const size_t off = b0 * per * eb, bytes = nb * per * eb;
+    cudaStream_t st = P->hs[ci];
+    CUDA_TRY(cudaMemcpyAsync(P->hbuf[ci].p, (const char*)h_in + off, bytes, cudaMemcpyHostToDevice, st));
+    ps.nrows = (long long)nb;
+    const bool inv = sign == TILEFFT_INVERSE;
+    int rc;
+    if (P->elem_bytes == 8) {
+      const float scale = inv ? 1.0f / (float)per : 1.0f;
+      rc = inv ? launch_fast<float, true>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, scale, st)
+               : launch_fast<float, false>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, scale, st);
+    } else {
+      const double scale = inv ? 1.0 / (double)per : 1.0;
+      rc = inv ? launch_fast<double, true>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, scale, st)
+               : launch_fast<double, false>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, scale, st);
+    }
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync((char*)h_out + off, P->hbuf[ci].p, bytes, cudaMemcpyDeviceToHost, st));
+  }
+  for (int i = 0; i < 3; ++i) CUDA_TRY(cudaStreamSynchronize(P->hs[i]));
+  return 0;
+}
+
+int tilefft_plan_destroy(tilefft_plan_t P) {
+  if (P) {
+    cudaSetDevice(P->device);
+    delete P;
+  }
+  return 0;
+}
+
+int tilefft_plan_info(tilefft_plan_t P, tilefft_plan_info_t* info) {
+  if (!P || !info) return fail(TILEFFT_EINVAL, "tilefft_plan_info: null argument");
+  std::memset(info, 0, sizeof(*info));
+  info->n = P->n;
+  info->batch = P->batch;
+  info->ny = P->ny;
+  info->nx = P->nx;
+  info->elem_bytes = P->elem_bytes;
+  info->mode = P->mode;
+  info->is_2d = P->is2d;
+  info->passes = (uint32_t)P->passes.size();
+  for (size_t i = 0; i < P->dev_factors.size() && i < 16; ++i) info->factors[i] = P->dev_factors[i];
+  info->launches_per_exec = (uint32_t)P->passes.size();
+  info->workspace_bytes = P->work.bytes;
+  info->table_bytes = P->tables.bytes;
+  return 0;
+}
+
+}  // extern "C"

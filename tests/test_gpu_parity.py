@@ -1,0 +1,158 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle.
+
+Tiers:
+  1. FAST mode: relative L2 <= 1e-5*log2(N) (fp32), 1e-12*log2(N) (fp64)
+     against the reference's fft_tiled on the same input (north-star tolerance).
+  2. EXACT mode: bit-identical to fft_tiled<Real> for the same plan and table.
+  3. PERMUTE mode: index maps bit-exact (ramp input, butterflies off).
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle_lib import rel_l2  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def tf():
+    import paper_1707_07263_b200 as tf
+    return tf
+
+
+def tol(n, dtype):
+    return (1e-5 if dtype == np.complex64 else 1e-12) * math.log2(n)
+
+
+def bits_equal(a, b):
+    return np.array_equal(np.ascontiguousarray(a).view(np.uint8), np.ascontiguousarray(b).view(np.uint8))
+
+
+# the 12 plans of test_tiled_fft.cpp:208-224 plus the BASELINE shapes (reduced where the oracle is slow)
+PLANS = [(2, 1024), (4, 2), (8, 4), (16, 4), (32, 2), (64, 4), (64, 8), (256, 16), (512, 8), (1024, 4),
+         (1024, 32), (1024, 1024), (4096, 64), (8192, 1024), (65536, 1024), (1 << 20, 1024), (1 << 20, 8192)]
+
+
+@pytest.mark.parametrize("n,cap", PLANS)
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_exact_mode_bit_identical(tf, oracle, n, cap, dtype):
+    x = oracle.random_bench_signal(n, 1).astype(dtype)
+    plan = tf.make_plan(n, cap)
+    table = tf.build_twiddle_table(n, dtype)
+    got = tf.fft_tiled(x, plan, table, mode="exact")
+    want = oracle.fft_tiled(x, cap)
+    assert bits_equal(got, want), f"n={n} cap={cap} rel={rel_l2(got, want)}"
+
+
+@pytest.mark.parametrize("n,cap", [(256, 16), (4096, 64), (1 << 16, 1024)])
+def test_exact_mode_inverse_bit_identical(tf, oracle, n, cap):
+    x = oracle.random_bench_signal(n, 2).astype(np.complex64)
+    plan = tf.make_plan(n, cap)
+    table = tf.build_twiddle_table(n, np.complex64)
+    assert bits_equal(tf.ifft_tiled(x, plan, table, mode="exact"), oracle.fft_tiled(x, cap, inverse=True))
+
+
+def test_exact_mode_larger_table_resolution(tf, oracle):
+    # the table may be finer than n (tiled_fft.hpp:328-329): values are resolution independent
+    n, cap, res = 4096, 64, 1 << 16
+    x = oracle.random_bench_signal(n, 5).astype(np.complex64)
+    got = tf.fft_tiled(x, tf.make_plan(n, cap), tf.build_twiddle_table(res, np.complex64), mode="exact")
+    assert bits_equal(got, oracle.fft_tiled(x, cap, res=res))
+
+
+def test_exact_mode_batched(tf, oracle):
+    n, cap, b = 1024, 32, 7
+    x = np.stack([oracle.random_signal(n, 100 + i) for i in range(b)]).astype(np.complex64)
+    got = tf.fft_tiled(x, tf.make_plan(n, cap), tf.build_twiddle_table(n, np.complex64), mode="exact")
+    assert bits_equal(got, oracle.fft_tiled(x, cap))
+
+
+@pytest.mark.parametrize("n,cap", [(16, 4), (8, 4), (64, 4), (4096, 64), (1 << 20, 1024)])
+def test_permute_mode_index_maps(tf, oracle, n, cap):
+    ramp = np.arange(n, dtype=np.float32).astype(np.complex64)
+    got = tf.fft_tiled(ramp, tf.make_plan(n, cap), None, mode="permute")
+    want = oracle.permute_tiled(ramp, cap)
+    assert bits_equal(got, want)
+    # and the permutation is the composition of the reference's maps
+    assert sorted(got.real.astype(np.int64).tolist()) == list(range(n))
+
+
+FAST_SIZES = [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 1 << 14, 1 << 15, 1 << 16, 1 << 17,
+              1 << 18, 1 << 20]
+
+
+@pytest.mark.parametrize("n", FAST_SIZES)
+def test_fast_mode_fp32_within_tolerance(tf, oracle, n):
+    x = oracle.random_bench_signal(n, 1).astype(np.complex64)
+    got = tf.fft_tiled(x, tf.make_plan(n))
+    want = oracle.fft_tiled(x)
+    err = rel_l2(got, want)
+    assert err <= tol(n, np.complex64), err
+    assert err < 5e-7, err  # much tighter than the contract: accurate roots
+
+
+@pytest.mark.parametrize("n", [2, 64, 1024, 8192, 1 << 14, 1 << 16, 1 << 20])
+def test_fast_mode_fp64_within_tolerance(tf, oracle, n):
+    x = oracle.random_bench_signal(n, 1)
+    got = tf.fft_tiled(x, tf.make_plan(n))
+    err = rel_l2(got, oracle.fft_tiled(x))
+    assert err <= tol(n, np.complex128), err
+
+
+@pytest.mark.parametrize("n", [1024, 1 << 16, 1 << 20])
+def test_fast_mode_inverse(tf, oracle, n):
+    x = oracle.random_bench_signal(n, 4).astype(np.complex64)
+    got = tf.ifft_tiled(x, tf.make_plan(n))
+    want = oracle.fft_tiled(x, inverse=True)
+    assert rel_l2(got, want) <= tol(n, np.complex64)
+    back = tf.ifft_tiled(tf.fft_tiled(x, tf.make_plan(n)), tf.make_plan(n))
+    assert rel_l2(back, x) <= tol(n, np.complex64)
+
+
+def test_fast_batched_1024_headline_shape(tf, oracle):
+    """configs[1]: batched 1024 x 65536 — every row against the oracle."""
+    n, b = 1024, 65536
+    x = oracle.random_bench_signal(n * b, 1).astype(np.complex64).reshape(b, n)
+    got = tf.fft_tiled(x, tf.make_plan(n))
+    want = oracle.fft_tiled(x)
+    assert rel_l2(got, want) <= tol(n, np.complex64)
+    per_row = np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)
+    assert per_row.max() < 1e-6
+
+
+def test_fast_device_path_matches_host_path(tf, oracle):
+    import torch
+    n, b = 1 << 20, 2
+    x = oracle.random_bench_signal(n * b, 9).astype(np.complex64).reshape(b, n)
+    host = tf.fft_tiled(x, tf.make_plan(n))
+    xd = torch.from_numpy(x).cuda()
+    dev = tf.fft_tiled_device(xd, tf.make_plan(n)).cpu().numpy()
+    assert bits_equal(host, dev)
+    # in place
+    tf.fft_tiled_device(xd, tf.make_plan(n), out=xd)
+    assert bits_equal(host, xd.cpu().numpy())
+
+
+def test_fast_2d_matches_rows_then_columns(tf, oracle):
+    for ny, nx in [(64, 32), (1024, 1024), (2048, 512), (16, 8192)]:
+        img = oracle.random_bench_signal(ny * nx, 3).astype(np.complex64).reshape(ny, nx)
+        got = tf.fft2_tiled(img)
+        want = oracle.fft2(img)
+        assert rel_l2(got, want) <= tol(ny * nx, np.complex64), (ny, nx)
+
+
+def test_fast_2d_inverse_roundtrip(tf, oracle):
+    img = oracle.random_bench_signal(4096 * 256, 3).astype(np.complex64).reshape(2, 2048, 256)
+    back = tf.fft2_tiled(tf.fft2_tiled(img), inverse=True)
+    assert rel_l2(back, img) <= tol(2048 * 256, np.complex64)
+
+
+def test_errors_match_reference(tf):
+    plan = tf.make_plan(256, 16)
+    x = np.zeros(128, np.complex64)
+    with pytest.raises(ValueError, match="signal length does not match the plan"):
+        tf.fft_tiled(x, plan)
+    with pytest.raises(ValueError, match="must divide the table resolution"):
+        tf.fft_tiled(np.zeros(256, np.complex64), plan, tf.build_twiddle_table(64, np.complex64))
