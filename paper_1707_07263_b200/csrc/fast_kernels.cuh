@@ -233,12 +233,15 @@ __device__ __forceinline__ long long final_index_dev(const CombArgs& a, long lon
   return out;
 }
 
+// Combs per CTA: one 128-byte line per comb step (16 fp32 / 8 fp64 elements).
+template <typename Real> struct FOf { static constexpr int v = 128 / (int)sizeof(C2<Real>); };
+
 template <typename Real, int L>
 struct CombCfg {
   using V = C2<Real>;
   static constexpr int RMAX = RmaxOf<Real>::v;
   using Sh = Shape<L, RMAX>;
-  static constexpr int F = 16;
+  static constexpr int F = FOf<Real>::v;
   static constexpr int THREADS = F * Sh::T;
   static constexpr int SMEM = (Sh::NST > 1 ? L * F : 1) * (int)sizeof(V);
 };
@@ -325,7 +328,7 @@ struct FinalCfg {
   using V = C2<Real>;
   static constexpr int RMAX = RmaxOf<Real>::v;
   using Sh = Shape<L, RMAX>;
-  static constexpr int F = 16;
+  static constexpr int F = FOf<Real>::v;
   static constexpr int THREADS = F * Sh::T;
   static constexpr int REG = L + L / 32 + 1;
   static constexpr int A = F * REG, B = L * (F + 1);

@@ -346,6 +346,7 @@ int launch_exact(const Pass& ps, const void* in, void* out, const void* tb, Real
 template <typename Real>
 int build_fast_1d(tilefft_plan_s* P, TableBuilder<Real>& tb) {
   const uint64_t n = P->n, B = P->batch;
+  constexpr uint64_t kF = tfb::FOf<Real>::v;
   if (n <= 8192) {
     Pass ps{};
     ps.kind = K_ROWS;
@@ -376,13 +377,13 @@ int build_fast_1d(tilefft_plan_s* P, TableBuilder<Real>& tb) {
       add_interpass(tb, g.sub_len[s], &ps.wc_off, &ps.wf_off, &fb);
       tfb::CombArgs& a = ps.comb;
       a.bstride = (long long)n;
-      a.chunks = (long long)(g.rps[s] / 16);
+      a.chunks = (long long)(g.rps[s] / kF);
       a.groups_per_batch = (long long)(n / g.sub_len[s]);
       a.ntiles = a.chunks * a.groups_per_batch * (long long)B;
       a.sub_len = (long long)g.sub_len[s];
       a.rps = (long long)g.rps[s];
       a.es = 1;
-      a.fvalid = 16;
+      a.fvalid = kF;
       a.fb = fb;
       a.m_mask = (uint32_t)(g.sub_len[s] - 1);
       a.p = (int)p;
@@ -396,7 +397,7 @@ int build_fast_1d(tilefft_plan_s* P, TableBuilder<Real>& tb) {
       a.bstride = (long long)n;
       a.n = (long long)n;
       a.sw0 = (long long)g.sub_w[0];
-      a.chunks = (long long)(f[0] / 16);
+      a.chunks = (long long)(f[0] / kF);
       a.ntiles = a.chunks * a.sw0 * (long long)B;
       a.out_w_last = (long long)g.out_w[p - 1];
       a.p = (int)p;
@@ -416,6 +417,7 @@ int build_fast_1d(tilefft_plan_s* P, TableBuilder<Real>& tb) {
 template <typename Real>
 int build_axis_passes(tilefft_plan_s* P, TableBuilder<Real>& tb, uint64_t ny, uint64_t nx, uint64_t B, int buf,
                       int dst) {
+  constexpr uint64_t kF = tfb::FOf<Real>::v;
   const std::vector<uint64_t> f = ny <= 1024 ? std::vector<uint64_t>{ny} : balanced_factors(ny, 1024);
   const Geo g = geometry(ny, f);
   const size_t p = f.size();
@@ -432,8 +434,8 @@ int build_axis_passes(tilefft_plan_s* P, TableBuilder<Real>& tb, uint64_t ny, ui
     int fb = 0;
     if (ps.twid) add_interpass(tb, g.sub_len[s], &ps.wc_off, &ps.wf_off, &fb);
     a.bstride = (long long)(ny * nx);
-    a.chunks = (long long)((nx + 15) / 16);
-    a.fvalid = (int)std::min<uint64_t>(16, nx);
+    a.chunks = (long long)((nx + kF - 1) / kF);
+    a.fvalid = (int)std::min<uint64_t>(kF, nx);
     a.groups_per_batch = (long long)(ny / f[s]);  // rows of this pass
     a.ntiles = a.chunks * a.groups_per_batch * (long long)B;
     a.sub_len = (long long)g.sub_len[s];
