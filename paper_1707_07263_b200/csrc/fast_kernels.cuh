@@ -22,6 +22,7 @@
 //     of copy bandwidth, 128-byte at 88%; profiles/r01_membench.txt).
 #pragma once
 #include "fft_common.cuh"
+#include "tma_util.cuh"
 
 namespace tfb {
 
@@ -189,6 +190,112 @@ k_rows(const C2<Real>* in, C2<Real>* out, long long nrows, const C2<Real>* __res
       if (scale != (Real)1) r = mk(r.x * scale, r.y * scale);
       dst[out_index<L, Cfg::RMAX>(t, j)] = r;
     }
+  }
+}
+
+// ------------------------------------------------------------------ K_ROWS_TMA
+// Persistent, TMA-staged variant of K_ROWS for rows that fit one warp
+// (T <= 32: L <= 1024 fp32, L <= 512 fp64). Each warp owns an S-deep ring of
+// shared-memory slots; lane 0 streams the warp's next chunks of rows into the
+// ring with 1D bulk copies (cp.async.bulk + mbarrier complete_tx) while the
+// warp computes the current chunk, so every SM keeps ~S-1 chunks of loads in
+// flight with no registers tied up. The slot doubles as the padded exchange
+// buffer of the Stockham stages; results leave straight from registers.
+template <int L, int T>
+struct RegionPad {
+  // per-FFT region >= L + L/32, == T (mod 16) so the FFTs that share a
+  // half-warp land on disjoint banks; even => 16-byte aligned regions
+  static constexpr int base = L + L / 32;
+  static constexpr int tm = T % 16;
+  static constexpr int v = base + ((tm - base % 16) + 16) % 16;
+};
+
+template <typename Real, int L, int WARPS, int S>
+struct RowsTmaCfg {
+  using V = C2<Real>;
+  static constexpr int RMAX = RmaxOf<Real>::v;
+  using Sh = Shape<L, RMAX>;
+  static_assert(Sh::T <= 32, "one warp per chunk");
+  static constexpr int FPW = 32 / Sh::T;                        // FFTs per warp chunk
+  static constexpr bool EXCH = Sh::NST > 1;
+  static constexpr int REG = EXCH ? RegionPad<L, Sh::T>::v : L;  // elements per FFT region
+  static constexpr int SLOT = FPW * REG;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int DATA_BYTES = WARPS * S * SLOT * (int)sizeof(V);
+  static constexpr int SMEM = DATA_BYTES + WARPS * S * 8;
+};
+
+template <typename Real, int L, int WARPS, int S, bool INV>
+__global__ void __launch_bounds__(WARPS * 32)
+k_rows_tma(const C2<Real>* in, C2<Real>* out, long long nrows, const C2<Real>* __restrict__ tw, Real scale) {
+  using Cfg = RowsTmaCfg<Real, L, WARPS, S>;
+  using V = C2<Real>;
+  using Sh = typename Cfg::Sh;
+  constexpr int FPW = Cfg::FPW;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ff = lane / Sh::T, tt = lane % Sh::T;
+  V* slots = reinterpret_cast<V*>(smem_raw) + (size_t)w * S * Cfg::SLOT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + Cfg::DATA_BYTES) + w * S;
+  const long long nchunks = (nrows + FPW - 1) / FPW;
+  const long long G = (long long)gridDim.x * WARPS;
+  long long c = (long long)blockIdx.x * WARPS + w;
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  auto issue = [&](long long chunk, int s) {
+    V* dst = slots + s * Cfg::SLOT;
+    const long long r0 = chunk * FPW;
+    const int nr = (int)((nrows - r0) < FPW ? (nrows - r0) : FPW);
+    mbar_arrive_expect_tx(&bars[s], (uint32_t)(nr * L * (int)sizeof(V)));
+    if constexpr (Cfg::EXCH) {
+      for (int f = 0; f < nr; ++f) tma_load_1d(dst + f * Cfg::REG, in + (r0 + f) * L, L * (int)sizeof(V), &bars[s]);
+    } else {
+      tma_load_1d(dst, in + r0 * L, (uint32_t)(nr * L * (int)sizeof(V)), &bars[s]);
+    }
+  };
+  if (lane == 0) {
+#pragma unroll 1
+    for (int s = 0; s < S - 1; ++s)
+      if (c + s * G < nchunks) issue(c + s * G, s);
+  }
+  int k = 0;
+#pragma unroll 1
+  for (; c < nchunks; c += G, ++k) {
+    const int s = k % S;
+    if (lane == 0) {
+      const long long cn = c + (long long)(S - 1) * G;
+      if (cn < nchunks) issue(cn, (k + S - 1) % S);
+    }
+    mbar_wait(&bars[s], (uint32_t)((k / S) & 1));
+    V* reg = slots + s * Cfg::SLOT + ff * Cfg::REG;
+    V v[Sh::R];
+#pragma unroll
+    for (int q = 0; q < Sh::R; ++q) v[q] = reg[tt + q * Sh::T];
+    if constexpr (Cfg::EXCH) {
+      __syncwarp();
+      auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
+      SyncWarp sy;
+      Stages<V, L, Cfg::RMAX, INV, 0>::run(v, tt, ex, tw, sy);
+    } else {
+      auto ex = [reg](int i) -> V& { return reg[i]; };
+      SyncWarp sy;
+      Stages<V, L, Cfg::RMAX, INV, 0>::run(v, tt, ex, tw, sy);
+    }
+    const long long row = c * FPW + ff;
+    if (row < nrows) {
+      V* dst = out + row * L;
+#pragma unroll
+      for (int j = 0; j < Sh::R; ++j) {
+        V r = v[j];
+        if (scale != (Real)1) r = mk(r.x * scale, r.y * scale);
+        dst[out_index<L, Cfg::RMAX>(tt, j)] = r;
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
   }
 }
 

@@ -103,6 +103,7 @@ struct Pass {
   size_t wc_off, wf_off;     // inter-pass tables
   bool twid;
   bool final_pass;           // the pass that applies the inverse scale
+  bool no_tma;               // force the register-only K_ROWS variant
 };
 
 }  // namespace
@@ -254,8 +255,39 @@ constexpr int rows_fpc(int L) {
   return f < 1 ? 1 : f;
 }
 
+// TMA-staged persistent rows kernel configuration (warps per CTA, ring depth)
+constexpr int kRowsWarps = 4;
+constexpr int kRowsStages = 2;
+
 template <typename Real, int L, bool INV>
 int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, Real scale, cudaStream_t st) {
+  constexpr int RM = tfb::RmaxOf<Real>::v;
+  constexpr int T = (L < RM ? 1 : L / RM);
+  const bool aligned = ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0) && (L * sizeof(tfb::C2<Real>)) % 16 == 0;
+  if constexpr (T <= 32) {
+    if (aligned && !ps.no_tma) {
+      using Cfg = tfb::RowsTmaCfg<Real, L, kRowsWarps, kRowsStages>;
+      auto k = tfb::k_rows_tma<Real, L, kRowsWarps, kRowsStages, INV>;
+      if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
+      static int blocks_per_sm[16] = {0};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      int& bps = blocks_per_sm[dev & 15];
+      if (!bps) {
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, Cfg::THREADS, Cfg::SMEM));
+        if (bps < 1) bps = 1;
+      }
+      int sms = 0;
+      CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const long long chunks = (ps.nrows + Cfg::FPW - 1) / Cfg::FPW;
+      const long long want = (chunks + kRowsWarps - 1) / kRowsWarps;
+      const long long grid = std::max<long long>(1, std::min<long long>(want, (long long)sms * bps));
+      k<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, st>>>((const tfb::C2<Real>*)in, (tfb::C2<Real>*)out, ps.nrows,
+                                                         (const tfb::C2<Real>*)tw + ps.tw_off, scale);
+      CUDA_TRY(cudaGetLastError());
+      return 0;
+    }
+  }
   constexpr int FPC = rows_fpc<Real>(L);
   using Cfg = tfb::RowsCfg<Real, L, FPC>;
   auto k = tfb::k_rows<Real, L, FPC, INV>;
