@@ -1,0 +1,61 @@
+// Host-side internals shared by the tilefft_b200 translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "exact_kernels.cuh"
+#include "fast_kernels.cuh"
+#include "../../include/tilefft_b200.h"
+
+namespace tfb_host {
+
+extern thread_local std::string g_err;
+int fail(int code, const char* fmt, ...);
+
+#define CUDA_TRY(expr)                                                                             \
+  do {                                                                                             \
+    cudaError_t e_ = (expr);                                                                       \
+    if (e_ != cudaSuccess) return ::tfb_host::fail(TILEFFT_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+// Opt a kernel into >48 KB dynamic shared memory (once per function/device).
+int ensure_smem(const void* fn, int bytes);
+
+enum PassKind { K_ROWS = 0, K_COMB1D = 1, K_COMBAX = 2, K_FINALT = 3, K_EXACT = 4 };
+
+struct Pass {
+  PassKind kind;
+  int L;
+  int src, dst;              // 0 = user input, 1 = user output, 2 = workspace
+  long long grid;
+  size_t smem;
+  tfb::CombArgs comb;
+  tfb::FinalArgs fin;
+  tfb::ExactArgs ex;
+  long long nrows;           // K_ROWS
+  size_t tw_off;             // offset (elements) of this L's Stockham table in the table buffer
+  size_t wc_off, wf_off;     // inter-pass tables
+  bool twid;
+  bool final_pass;           // the pass that applies the inverse scale
+  bool no_tma;               // force the register-only K_ROWS variant
+};
+
+// Kernel launchers, explicitly instantiated in kern_*.cu (one TU per
+// precision/direction so the heavy template instantiation builds in parallel).
+template <typename Real, bool INV>
+int launch_fast(const Pass& ps, const void* in, void* out, const void* tb, Real scale, cudaStream_t st);
+template <typename Real>
+int launch_exact(const Pass& ps, const void* in, void* out, const void* tb, Real scale, int conj_in, int conj_out,
+                 cudaStream_t st);
+
+extern template int launch_fast<float, false>(const Pass&, const void*, void*, const void*, float, cudaStream_t);
+extern template int launch_fast<float, true>(const Pass&, const void*, void*, const void*, float, cudaStream_t);
+extern template int launch_fast<double, false>(const Pass&, const void*, void*, const void*, double, cudaStream_t);
+extern template int launch_fast<double, true>(const Pass&, const void*, void*, const void*, double, cudaStream_t);
+extern template int launch_exact<float>(const Pass&, const void*, void*, const void*, float, int, int, cudaStream_t);
+extern template int launch_exact<double>(const Pass&, const void*, void*, const void*, double, int, int,
+                                         cudaStream_t);
+
+}  // namespace tfb_host

@@ -1,0 +1,6 @@
+// Fast-mode kernel instantiations: float, forward.
+#include "launch.cuh"
+
+namespace tfb_host {
+template int launch_fast<float, false>(const Pass&, const void*, void*, const void*, float, cudaStream_t);
+}  // namespace tfb_host

@@ -1,0 +1,6 @@
+// Fast-mode kernel instantiations: double, forward.
+#include "launch.cuh"
+
+namespace tfb_host {
+template int launch_fast<double, false>(const Pass&, const void*, void*, const void*, double, cudaStream_t);
+}  // namespace tfb_host

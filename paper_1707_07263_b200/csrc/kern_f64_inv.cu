@@ -1,0 +1,6 @@
+// Fast-mode kernel instantiations: double, inverse.
+#include "launch.cuh"
+
+namespace tfb_host {
+template int launch_fast<double, true>(const Pass&, const void*, void*, const void*, double, cudaStream_t);
+}  // namespace tfb_host

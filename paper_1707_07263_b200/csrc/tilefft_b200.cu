@@ -18,11 +18,9 @@
 #include <utility>
 #include <vector>
 
-#include "../../include/tilefft_b200.h"
-#include "exact_kernels.cuh"
-#include "fast_kernels.cuh"
+#include "internal.h"
 
-namespace {
+namespace tfb_host {
 
 thread_local std::string g_err;
 
@@ -36,11 +34,30 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
-#define CUDA_TRY(expr)                                                                    \
-  do {                                                                                    \
-    cudaError_t e_ = (expr);                                                              \
-    if (e_ != cudaSuccess) return fail(TILEFFT_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
-  } while (0)
+std::mutex g_attr_mu;
+struct AttrRec { const void* fn; int dev; int bytes; };
+std::vector<AttrRec> g_attr_done;
+int ensure_smem(const void* fn, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  for (auto& r : g_attr_done)
+    if (r.fn == fn && r.dev == dev) {
+      if (r.bytes >= bytes) return 0;
+      CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      r.bytes = bytes;
+      return 0;
+    }
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  g_attr_done.push_back({fn, dev, bytes});
+  return 0;
+}
+
+}  // namespace tfb_host
+
+using namespace tfb_host;
+
+namespace {
 
 bool is_pow2(uint64_t v) { return v != 0 && (v & (v - 1)) == 0; }
 int ilog2(uint64_t v) { return 63 - __builtin_clzll(v); }
@@ -85,25 +102,6 @@ struct DevBuf {
     bytes = b;
     return 0;
   }
-};
-
-enum PassKind { K_ROWS = 0, K_COMB1D = 1, K_COMBAX = 2, K_FINALT = 3, K_EXACT = 4 };
-
-struct Pass {
-  PassKind kind;
-  int L;
-  int src, dst;              // 0 = user input, 1 = user output, 2 = workspace
-  long long grid;
-  size_t smem;
-  tfb::CombArgs comb;
-  tfb::FinalArgs fin;
-  tfb::ExactArgs ex;
-  long long nrows;           // K_ROWS
-  size_t tw_off;             // offset (elements) of this L's Stockham table in the table buffer
-  size_t wc_off, wf_off;     // inter-pass tables
-  bool twid;
-  bool final_pass;           // the pass that applies the inverse scale
-  bool no_tma;               // force the register-only K_ROWS variant
 };
 
 }  // namespace
@@ -222,156 +220,6 @@ std::vector<uint64_t> balanced_factors(uint64_t n, uint64_t cap) {
   std::vector<uint64_t> f;
   for (int s = 0; s < p; ++s) f.push_back(1ull << (base + (s < extra ? 1 : 0)));
   return f;
-}
-
-// ---------------------------------------------------------------- kernel dispatch
-// Opt a kernel into >48 KB dynamic shared memory once per (function, device).
-std::mutex g_attr_mu;
-struct AttrRec { const void* fn; int dev; int bytes; };
-std::vector<AttrRec> g_attr_done;
-int ensure_smem(const void* fn, int bytes) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(g_attr_mu);
-  for (auto& r : g_attr_done)
-    if (r.fn == fn && r.dev == dev) {
-      if (r.bytes >= bytes) return 0;
-      CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      r.bytes = bytes;
-      return 0;
-    }
-  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  g_attr_done.push_back({fn, dev, bytes});
-  return 0;
-}
-
-// FFTs per CTA for K_ROWS: 8 warps of work for L <= 1024 (fp32), one FFT per CTA above.
-template <typename Real>
-constexpr int rows_fpc(int L) {
-  constexpr int RM = tfb::RmaxOf<Real>::v;
-  if (L >= 2048) return 1;
-  const int T = L < RM ? 1 : L / RM;
-  const int f = 256 / T;
-  return f < 1 ? 1 : f;
-}
-
-// TMA-staged persistent rows kernel configuration (warps per CTA, ring depth)
-constexpr int kRowsWarps = 4;
-constexpr int kRowsStages = 2;
-
-template <typename Real, int L, bool INV>
-int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, Real scale, cudaStream_t st) {
-  constexpr int RM = tfb::RmaxOf<Real>::v;
-  constexpr int T = (L < RM ? 1 : L / RM);
-  const bool aligned = ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0) && (L * sizeof(tfb::C2<Real>)) % 16 == 0;
-  if constexpr (T <= 32) {
-    if (aligned && !ps.no_tma) {
-      using Cfg = tfb::RowsTmaCfg<Real, L, kRowsWarps, kRowsStages>;
-      auto k = tfb::k_rows_tma<Real, L, kRowsWarps, kRowsStages, INV>;
-      if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
-      static int blocks_per_sm[16] = {0};
-      int dev = 0;
-      cudaGetDevice(&dev);
-      int& bps = blocks_per_sm[dev & 15];
-      if (!bps) {
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, Cfg::THREADS, Cfg::SMEM));
-        if (bps < 1) bps = 1;
-      }
-      int sms = 0;
-      CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      const long long chunks = (ps.nrows + Cfg::FPW - 1) / Cfg::FPW;
-      const long long want = (chunks + kRowsWarps - 1) / kRowsWarps;
-      const long long grid = std::max<long long>(1, std::min<long long>(want, (long long)sms * bps));
-      k<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, st>>>((const tfb::C2<Real>*)in, (tfb::C2<Real>*)out, ps.nrows,
-                                                         (const tfb::C2<Real>*)tw + ps.tw_off, scale);
-      CUDA_TRY(cudaGetLastError());
-      return 0;
-    }
-  }
-  constexpr int FPC = rows_fpc<Real>(L);
-  using Cfg = tfb::RowsCfg<Real, L, FPC>;
-  auto k = tfb::k_rows<Real, L, FPC, INV>;
-  if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
-  const long long grid = (ps.nrows + FPC - 1) / FPC;
-  k<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, st>>>((const tfb::C2<Real>*)in, (tfb::C2<Real>*)out, ps.nrows,
-                                                     (const tfb::C2<Real>*)tw + ps.tw_off, scale);
-  CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
-template <typename Real, int L, bool INV>
-int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, Real scale, cudaStream_t st) {
-  using Cfg = tfb::CombCfg<Real, L>;
-  using V = tfb::C2<Real>;
-  const V* t = (const V*)tb;
-  auto go = [&](auto k) -> int {
-    if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
-    k<<<(unsigned)ps.grid, Cfg::THREADS, Cfg::SMEM, st>>>((const V*)in, (V*)out, ps.comb, t + ps.tw_off,
-                                                          t + ps.wc_off, t + ps.wf_off, scale);
-    CUDA_TRY(cudaGetLastError());
-    return 0;
-  };
-  if (ps.kind == K_COMB1D) return go(tfb::k_comb<Real, L, INV, true, 0>);
-  if (ps.twid) return go(tfb::k_comb<Real, L, INV, true, 1>);
-  return go(tfb::k_comb<Real, L, INV, false, 1>);
-}
-
-template <typename Real, int L, bool INV>
-int launch_final(const Pass& ps, const void* in, void* out, const void* tb, Real scale, cudaStream_t st) {
-  using Cfg = tfb::FinalCfg<Real, L>;
-  using V = tfb::C2<Real>;
-  auto k = tfb::k_final_t<Real, L, INV>;
-  if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
-  k<<<(unsigned)ps.grid, Cfg::THREADS, Cfg::SMEM, st>>>((const V*)in, (V*)out, ps.fin, (const V*)tb + ps.tw_off,
-                                                        scale);
-  CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
-template <typename Real, bool INV>
-int launch_fast(const Pass& ps, const void* in, void* out, const void* tb, Real scale, cudaStream_t st) {
-#define DISPATCH(FN, ...)                                                     \
-  switch (ps.L) {                                                             \
-    case 2: return FN<Real, 2, INV>(ps, in, out, tb, scale, st);              \
-    case 4: return FN<Real, 4, INV>(ps, in, out, tb, scale, st);              \
-    case 8: return FN<Real, 8, INV>(ps, in, out, tb, scale, st);              \
-    case 16: return FN<Real, 16, INV>(ps, in, out, tb, scale, st);            \
-    case 32: return FN<Real, 32, INV>(ps, in, out, tb, scale, st);            \
-    case 64: return FN<Real, 64, INV>(ps, in, out, tb, scale, st);            \
-    case 128: return FN<Real, 128, INV>(ps, in, out, tb, scale, st);          \
-    case 256: return FN<Real, 256, INV>(ps, in, out, tb, scale, st);          \
-    case 512: return FN<Real, 512, INV>(ps, in, out, tb, scale, st);          \
-    case 1024: return FN<Real, 1024, INV>(ps, in, out, tb, scale, st);        \
-    __VA_ARGS__                                                               \
-  }
-  if (ps.kind == K_ROWS) {
-    DISPATCH(launch_rows,
-             case 2048: return launch_rows<Real, 2048, INV>(ps, in, out, tb, scale, st);
-             case 4096: return launch_rows<Real, 4096, INV>(ps, in, out, tb, scale, st);
-             case 8192: return launch_rows<Real, 8192, INV>(ps, in, out, tb, scale, st);)
-  } else if (ps.kind == K_COMB1D || ps.kind == K_COMBAX) {
-    DISPATCH(launch_comb)
-  } else if (ps.kind == K_FINALT) {
-    DISPATCH(launch_final)
-  }
-#undef DISPATCH
-  return fail(TILEFFT_EINVAL, "internal: no kernel for pass length %d", ps.L);
-}
-
-template <typename Real>
-int launch_exact(const Pass& ps, const void* in, void* out, const void* tb, Real scale, int conj_in, int conj_out,
-                 cudaStream_t st) {
-  using V = tfb::C2<Real>;
-  tfb::ExactArgs a = ps.ex;
-  a.conj_in = conj_in;
-  a.conj_scale_out = conj_out;
-  auto k = tfb::k_exact_pass<Real>;
-  const size_t smem = (size_t)a.L * sizeof(V);
-  if (int rc = ensure_smem((const void*)k, (int)smem)) return rc;
-  int threads = (int)std::min<long long>(256, std::max<long long>(32, a.L / 2));
-  k<<<(unsigned)ps.grid, threads, smem, st>>>((const V*)in, (V*)out, a, (const V*)tb, scale);
-  CUDA_TRY(cudaGetLastError());
-  return 0;
 }
 
 // ---------------------------------------------------------------- plan building
