@@ -47,6 +47,9 @@ extern "C" {
 #define TILEFFT_MODE_FAST 0
 #define TILEFFT_MODE_EXACT 1
 #define TILEFFT_MODE_PERMUTE 2
+#define TILEFFT_MODE_LEVELWISE 3  /* fft_levelwise (fft_baseline.hpp:66-116): bit reversal + one launch
+                                     per radix-2 level in global memory, bit-identical; the paper's
+                                     "previous method", kept for the §2.2-vs-§2.3 comparison */
 
 #define TILEFFT_FORWARD (-1)
 #define TILEFFT_INVERSE (+1)
@@ -97,6 +100,19 @@ typedef struct {
   uint64_t table_bytes;        /* device twiddle tables held by the plan */
 } tilefft_plan_info_t;
 TILEFFT_API int tilefft_plan_info(tilefft_plan_t plan, tilefft_plan_info_t* info);
+
+/* exchange_transpose (tiled_fft.hpp:179-203): out[exchange_index_map(stage,
+ * q)] = in[q] for the plan with `factors` (stage_plan.hpp:161-172), on the GPU,
+ * host buffers. */
+TILEFFT_API int tilefft_exchange(const void* h_in, void* h_out, uint64_t n, const uint64_t* factors,
+                                 uint32_t nfactors, uint32_t stage, uint32_t elem_bytes, int device);
+
+/* apply_interstage_twiddles (tiled_fft.hpp:153-172): element (r, k) of a
+ * rows x cols tile times W_{sub_len}^{((row0 + r) % rows_per_sub) * k} taken
+ * from the caller's table (bit-identical), on the GPU, host buffers. */
+TILEFFT_API int tilefft_interstage_scale(const void* h_in, void* h_out, uint64_t rows, uint64_t cols, uint64_t row0,
+                                         uint64_t rows_per_sub, uint64_t sub_len, const void* table,
+                                         uint64_t resolution, uint32_t elem_bytes, int device);
 
 /* Host-side root table with the reference's construction: entry j =
  * exp(-2 pi i j / resolution), interleaved, elem_bytes 8 or 16

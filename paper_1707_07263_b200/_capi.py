@@ -24,6 +24,7 @@ ENCCL = 1002
 MODE_FAST = 0
 MODE_EXACT = 1
 MODE_PERMUTE = 2
+MODE_LEVELWISE = 3
 FORWARD = -1
 INVERSE = +1
 
@@ -54,6 +55,8 @@ EXPORTS = (
     "tilefft_plan_destroy",
     "tilefft_plan_info",
     "tilefft_build_twiddle",
+    "tilefft_exchange",
+    "tilefft_interstage_scale",
     "tilefft_last_error",
     "tilefft_version",
 )
@@ -89,10 +92,13 @@ def load() -> ctypes.CDLL:
         lib.tilefft_plan_destroy.argtypes = [vp]
         lib.tilefft_plan_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
         lib.tilefft_build_twiddle.argtypes = [u64, u32, vp]
+        lib.tilefft_exchange.argtypes = [vp, vp, u64, ctypes.POINTER(u64), u32, u32, u32, i32]
+        lib.tilefft_interstage_scale.argtypes = [vp, vp, u64, u64, u64, u64, u64, vp, u64, u32, i32]
         lib.tilefft_last_error.restype = ctypes.c_char_p
         lib.tilefft_version.restype = ctypes.c_char_p
         for name in ("tilefft_plan_create", "tilefft_plan_create_2d", "tilefft_exec_c2c", "tilefft_exec_c2c_host",
-                     "tilefft_plan_destroy", "tilefft_plan_info", "tilefft_build_twiddle"):
+                     "tilefft_plan_destroy", "tilefft_plan_info", "tilefft_build_twiddle", "tilefft_exchange",
+                     "tilefft_interstage_scale"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
         return lib
@@ -149,7 +155,7 @@ class DevicePlan:
         pi = PlanInfo()
         check(self._lib.tilefft_plan_info(self._h, ctypes.byref(pi)))
         d = {k: getattr(pi, k) for k, _ in PlanInfo._fields_ if k != "factors"}
-        d["factors"] = [int(pi.factors[i]) for i in range(pi.passes)]
+        d["factors"] = [int(pi.factors[i]) for i in range(min(pi.passes, 16))]
         return d
 
     def close(self) -> None:
@@ -162,6 +168,19 @@ class DevicePlan:
             self.close()
         except Exception:
             pass
+
+
+def exchange(h_in: int, h_out: int, n: int, factors, stage: int, elem_bytes: int, device: int = 0) -> None:
+    fac = (ctypes.c_uint64 * len(factors))(*[int(f) for f in factors])
+    check(load().tilefft_exchange(ctypes.c_void_p(h_in), ctypes.c_void_p(h_out), int(n), fac, len(factors),
+                                  int(stage), int(elem_bytes), int(device)))
+
+
+def interstage_scale(h_in: int, h_out: int, rows: int, cols: int, row0: int, rows_per_sub: int, sub_len: int,
+                     table_ptr: int, resolution: int, elem_bytes: int, device: int = 0) -> None:
+    check(load().tilefft_interstage_scale(ctypes.c_void_p(h_in), ctypes.c_void_p(h_out), int(rows), int(cols),
+                                          int(row0), int(rows_per_sub), int(sub_len), ctypes.c_void_p(table_ptr),
+                                          int(resolution), int(elem_bytes), int(device)))
 
 
 def build_twiddle(resolution: int, elem_bytes: int, out_ptr: int) -> None:

@@ -99,4 +99,92 @@ __global__ void k_exact_pass(const C2<Real>* in, C2<Real>* out, ExactArgs a, con
   }
 }
 
+// ---------------------------------------------------------------- levelwise
+// The paper's "previous method" (§2.2; fft_levelwise,
+// fft_baseline.hpp:66-116): one bit-reversal sweep, then one launch per
+// radix-2 level, each reading and writing all n elements in global memory.
+// Same table roots and separately rounded ops as the reference, so the output
+// is bit-identical to fft_levelwise<Real>.
+template <typename Real>
+__global__ void k_bitrev_permute(const C2<Real>* in, C2<Real>* out, long long n, int bits, long long total,
+                                 int conj_in) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / n, j = i % n;
+    const unsigned long long r = __brevll((unsigned long long)j) >> (64 - bits);
+    C2<Real> x = in[b * n + (long long)r];
+    if (conj_in) x.y = -x.y;
+    out[i] = x;
+  }
+}
+
+template <typename Real>
+__global__ void k_level(C2<Real>* w, long long n, int lv, long long total_half, const C2<Real>* __restrict__ tbl,
+                        int conj_scale_out, Real scale) {
+  using V = C2<Real>;
+  const long long h = 1LL << lv;
+  const long long tstride = n / (2 * h);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total_half;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / (n / 2), k = i % (n / 2);
+    const long long j = k & (h - 1);
+    const long long lo = b * n + ((k >> lv) << (lv + 1)) + j, hi = lo + h;
+    const V wv = tbl[j * tstride];
+    const V bv = w[hi], av = w[lo];
+    const Real tr = rn_sub(rn_mul(wv.x, bv.x), rn_mul(wv.y, bv.y));
+    const Real ti = rn_add(rn_mul(wv.x, bv.y), rn_mul(wv.y, bv.x));
+    V a = mk(rn_add(av.x, tr), rn_add(av.y, ti)), c = mk(rn_sub(av.x, tr), rn_sub(av.y, ti));
+    if (conj_scale_out) {
+      a = mk(rn_mul(a.x, scale), rn_mul(-a.y, scale));
+      c = mk(rn_mul(c.x, scale), rn_mul(-c.y, scale));
+    }
+    w[lo] = a;
+    w[hi] = c;
+  }
+}
+
+// Decomposed helpers of the reference API (tiled_fft.hpp:153-203), exact:
+// element (r, k) of a rows x cols tile times W_sub^{((row0+r) % rps) * k}
+// (element as left operand), and the stage store permutation.
+template <typename Real>
+__global__ void k_interstage_scale(const C2<Real>* in, C2<Real>* out, long long rows, long long cols, long long row0,
+                                   long long rps, long long sub_len, const C2<Real>* __restrict__ tbl,
+                                   long long tstride) {
+  const long long total = rows * cols;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = ((row0 + i / cols) % rps), k = i % cols;
+    const unsigned long long e = ((unsigned long long)r * (unsigned long long)k) & (unsigned long long)(sub_len - 1);
+    const C2<Real> w = tbl[(long long)e * tstride], x = in[i];
+    out[i] = mk(rn_sub(rn_mul(x.x, w.x), rn_mul(x.y, w.y)), rn_add(rn_mul(x.x, w.y), rn_mul(x.y, w.x)));
+  }
+}
+
+struct ExchangeArgs {
+  long long n, L, sub_len, rps;
+  int final_pass, p;
+  long long out_w[64], sub_w[64];
+};
+
+// out[exchange_index_map(stage, q)] = in[q] (stage_plan.hpp:161-172)
+template <typename Real>
+__global__ void k_exchange(const C2<Real>* in, C2<Real>* out, ExchangeArgs a) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < a.n; q += (long long)gridDim.x * blockDim.x) {
+    long long dst;
+    if (!a.final_pass) {
+      const long long sub = q / a.sub_len, local = q % a.sub_len;
+      dst = sub * a.sub_len + (local % a.L) * a.rps + local / a.L;
+    } else {
+      long long rem = q / a.L;
+      dst = (q % a.L) * a.out_w[a.p - 1];
+      for (int i = 0; i + 1 < a.p; ++i) {
+        const long long d = rem / a.sub_w[i];
+        rem -= d * a.sub_w[i];
+        dst += d * a.out_w[i];
+      }
+    }
+    out[dst] = in[q];
+  }
+}
+
 }  // namespace tfb

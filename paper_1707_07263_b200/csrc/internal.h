@@ -23,7 +23,7 @@ int fail(int code, const char* fmt, ...);
 // Opt a kernel into >48 KB dynamic shared memory (once per function/device).
 int ensure_smem(const void* fn, int bytes);
 
-enum PassKind { K_ROWS = 0, K_COMB1D = 1, K_COMBAX = 2, K_FINALT = 3, K_EXACT = 4 };
+enum PassKind { K_ROWS = 0, K_COMB1D = 1, K_COMBAX = 2, K_FINALT = 3, K_EXACT = 4, K_BITREV = 5, K_LEVEL = 6 };
 
 struct Pass {
   PassKind kind;
@@ -40,6 +40,8 @@ struct Pass {
   bool twid;
   bool final_pass;           // the pass that applies the inverse scale
   bool no_tma;               // force the register-only K_ROWS variant
+  int level;                 // K_LEVEL: radix-2 level (h = 2^level)
+  long long lw_n, lw_total;  // K_BITREV/K_LEVEL: transform length, elements (or half) in the batch
 };
 
 // Kernel launchers, explicitly instantiated in kern_*.cu (one TU per
@@ -50,11 +52,30 @@ template <typename Real>
 int launch_exact(const Pass& ps, const void* in, void* out, const void* tb, Real scale, int conj_in, int conj_out,
                  cudaStream_t st);
 
+template <typename Real>
+int launch_levelwise(const Pass& ps, const void* in, void* out, const void* tb, Real scale, int conj_in, int conj_out,
+                     cudaStream_t st);
+template <typename Real>
+int launch_exchange(const void* in, void* out, const tfb::ExchangeArgs& a, cudaStream_t st);
+template <typename Real>
+int launch_interstage(const void* in, void* out, long long rows, long long cols, long long row0, long long rps,
+                      long long sub_len, const void* tbl, long long tstride, cudaStream_t st);
+
 extern template int launch_fast<float, false>(const Pass&, const void*, void*, const void*, float, cudaStream_t);
 extern template int launch_fast<float, true>(const Pass&, const void*, void*, const void*, float, cudaStream_t);
 extern template int launch_fast<double, false>(const Pass&, const void*, void*, const void*, double, cudaStream_t);
 extern template int launch_fast<double, true>(const Pass&, const void*, void*, const void*, double, cudaStream_t);
 extern template int launch_exact<float>(const Pass&, const void*, void*, const void*, float, int, int, cudaStream_t);
+extern template int launch_levelwise<float>(const Pass&, const void*, void*, const void*, float, int, int,
+                                           cudaStream_t);
+extern template int launch_levelwise<double>(const Pass&, const void*, void*, const void*, double, int, int,
+                                            cudaStream_t);
+extern template int launch_exchange<float>(const void*, void*, const tfb::ExchangeArgs&, cudaStream_t);
+extern template int launch_exchange<double>(const void*, void*, const tfb::ExchangeArgs&, cudaStream_t);
+extern template int launch_interstage<float>(const void*, void*, long long, long long, long long, long long, long long,
+                                            const void*, long long, cudaStream_t);
+extern template int launch_interstage<double>(const void*, void*, long long, long long, long long, long long,
+                                             long long, const void*, long long, cudaStream_t);
 extern template int launch_exact<double>(const Pass&, const void*, void*, const void*, double, int, int,
                                          cudaStream_t);
 

@@ -135,4 +135,43 @@ int launch_exact(const Pass& ps, const void* in, void* out, const void* tb, Real
   return 0;
 }
 
+template <typename Real>
+int launch_levelwise(const Pass& ps, const void* in, void* out, const void* tb, Real scale, int conj_in, int conj_out,
+                     cudaStream_t st) {
+  using V = tfb::C2<Real>;
+  const int threads = 256;
+  if (ps.kind == K_BITREV) {
+    const long long blocks = std::min<long long>((ps.lw_total + threads - 1) / threads, 148LL * 16);
+    tfb::k_bitrev_permute<Real><<<(unsigned)blocks, threads, 0, st>>>((const V*)in, (V*)out, ps.lw_n,
+                                                                     (int)(63 - __builtin_clzll(ps.lw_n)),
+                                                                     ps.lw_total, conj_in);
+  } else {
+    const long long blocks = std::min<long long>((ps.lw_total + threads - 1) / threads, 148LL * 16);
+    tfb::k_level<Real><<<(unsigned)blocks, threads, 0, st>>>((V*)out, ps.lw_n, ps.level, ps.lw_total, (const V*)tb,
+                                                            conj_out, scale);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <typename Real>
+int launch_exchange(const void* in, void* out, const tfb::ExchangeArgs& a, cudaStream_t st) {
+  using V = tfb::C2<Real>;
+  const long long blocks = std::min<long long>((a.n + 255) / 256, 148LL * 16);
+  tfb::k_exchange<Real><<<(unsigned)blocks, 256, 0, st>>>((const V*)in, (V*)out, a);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <typename Real>
+int launch_interstage(const void* in, void* out, long long rows, long long cols, long long row0, long long rps,
+                      long long sub_len, const void* tbl, long long tstride, cudaStream_t st) {
+  using V = tfb::C2<Real>;
+  const long long blocks = std::min<long long>((rows * cols + 255) / 256, 148LL * 16);
+  tfb::k_interstage_scale<Real><<<(unsigned)blocks, 256, 0, st>>>((const V*)in, (V*)out, rows, cols, row0, rps,
+                                                                 sub_len, (const V*)tbl, tstride);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 }  // namespace tfb_host

@@ -388,6 +388,47 @@ int build_exact(tilefft_plan_s* P, TableBuilder<Real>& tb, const std::vector<uin
   return 0;
 }
 
+// The paper's previous method: bit reversal + one launch per radix-2 level
+// (fft_levelwise, fft_baseline.hpp:66-116). Roots W_n^e from the caller's table.
+template <typename Real>
+int build_levelwise(tilefft_plan_s* P, TableBuilder<Real>& tb, const void* tv, uint64_t tres) {
+  const uint64_t n = P->n;
+  const size_t off = tb.add(n);
+  for (uint64_t e = 0; e < n; ++e) {
+    Real re, im;
+    if (tv) {
+      const Real* v = (const Real*)tv;
+      const uint64_t stride = tres / n;
+      re = v[2 * e * stride];
+      im = v[2 * e * stride + 1];
+    } else {
+      ref_root<Real>(e, n, &re, &im);
+    }
+    tb.set(off + e, re, im);
+  }
+  Pass ps{};
+  ps.kind = K_BITREV;
+  ps.src = 0;
+  ps.dst = 1;
+  ps.lw_n = (long long)n;
+  ps.lw_total = (long long)(n * P->batch);
+  P->passes.push_back(ps);
+  const int levels = ilog2(n);
+  for (int lv = 0; lv < levels; ++lv) {
+    Pass q{};
+    q.kind = K_LEVEL;
+    q.src = 1;
+    q.dst = 1;
+    q.level = lv;
+    q.lw_n = (long long)n;
+    q.lw_total = (long long)(n / 2 * P->batch);
+    q.final_pass = lv + 1 == levels;
+    P->passes.push_back(q);
+  }
+  P->dev_factors.assign((size_t)levels, 2);
+  return 0;
+}
+
 int check_device(int device) {
   int count = 0;
   cudaError_t e = cudaGetDeviceCount(&count);
@@ -435,6 +476,9 @@ int exec_impl(tilefft_plan_s* P, const void* in, void* out, int sign, cudaStream
     if (ps.kind == K_EXACT) {
       const bool first = &ps == &P->passes.front();
       rc = launch_exact<Real>(ps, src, dst, P->tables.p, scale, inv && first, inv && ps.final_pass, st);
+    } else if (ps.kind == K_BITREV || ps.kind == K_LEVEL) {
+      rc = launch_levelwise<Real>(ps, src, dst, P->tables.p, scale, inv && ps.kind == K_BITREV,
+                                  inv && ps.final_pass, st);
     } else if (inv) {
       rc = launch_fast<Real, true>(ps, src, dst, P->tables.p, ps.final_pass ? scale : (Real)1, st);
     } else {
@@ -445,6 +489,21 @@ int exec_impl(tilefft_plan_s* P, const void* in, void* out, int sign, cudaStream
   return 0;
 }
 
+}  // namespace
+
+namespace {
+// run `fn(d_in, d_out)` on temporary device copies of host buffers
+template <class F>
+int with_device_buffers(int device, const void* h_in, void* h_out, size_t in_bytes, size_t out_bytes, F fn) {
+  if (int rc = check_device(device)) return rc;
+  DevBuf din, dout;
+  if (int rc = din.alloc(in_bytes)) return rc;
+  if (int rc = dout.alloc(out_bytes)) return rc;
+  CUDA_TRY(cudaMemcpy(din.p, h_in, in_bytes, cudaMemcpyHostToDevice));
+  if (int rc = fn(din.p, dout.p)) return rc;
+  CUDA_TRY(cudaMemcpy(h_out, dout.p, out_bytes, cudaMemcpyDeviceToHost));
+  return 0;
+}
 }  // namespace
 
 // ================================================================ C ABI
@@ -479,7 +538,7 @@ int tilefft_plan_create(tilefft_plan_t* out, uint64_t n, uint64_t batch, const u
   if (!is_pow2(n) || n < 2) return fail(TILEFFT_EINVAL, "make_plan: n must be a power of two >= 2");
   if (batch < 1) return fail(TILEFFT_EINVAL, "tilefft_plan_create: batch must be >= 1");
   if (elem_bytes != 8 && elem_bytes != 16) return fail(TILEFFT_EINVAL, "tilefft_plan_create: elem_bytes must be 8 or 16");
-  if (mode > TILEFFT_MODE_PERMUTE) return fail(TILEFFT_EINVAL, "tilefft_plan_create: unknown mode %u", mode);
+  if (mode > TILEFFT_MODE_LEVELWISE) return fail(TILEFFT_EINVAL, "tilefft_plan_create: unknown mode %u", mode);
   std::vector<uint64_t> f;
   if (factors && nfactors) {
     uint64_t prod = 1;
@@ -490,8 +549,9 @@ int tilefft_plan_create(tilefft_plan_t* out, uint64_t n, uint64_t batch, const u
     }
     if (prod != n) return fail(TILEFFT_EINVAL, "fft_tiled: signal length does not match the plan");
   }
-  if (mode != TILEFFT_MODE_FAST && f.empty()) return fail(TILEFFT_EINVAL, "fft_tiled: empty plan");
-  if (mode == TILEFFT_MODE_EXACT && tv != nullptr &&
+  if ((mode == TILEFFT_MODE_EXACT || mode == TILEFFT_MODE_PERMUTE) && f.empty())
+    return fail(TILEFFT_EINVAL, "fft_tiled: empty plan");
+  if ((mode == TILEFFT_MODE_EXACT || mode == TILEFFT_MODE_LEVELWISE) && tv != nullptr &&
       !(tres >= n && is_pow2(tres) && tres % n == 0))
     return fail(TILEFFT_EINVAL, "fft_tiled: signal length must divide the table resolution");
   if (int rc = check_device(device)) return rc;
@@ -505,11 +565,15 @@ int tilefft_plan_create(tilefft_plan_t* out, uint64_t n, uint64_t batch, const u
   int rc;
   if (elem_bytes == 8) {
     TableBuilder<float> tb;
-    rc = mode == TILEFFT_MODE_FAST ? build_fast_1d<float>(P, tb) : build_exact<float>(P, tb, f, tv, tres);
+    rc = mode == TILEFFT_MODE_FAST        ? build_fast_1d<float>(P, tb)
+         : mode == TILEFFT_MODE_LEVELWISE ? build_levelwise<float>(P, tb, tv, tres)
+                                          : build_exact<float>(P, tb, f, tv, tres);
     if (!rc) rc = finish_plan<float>(P, tb);
   } else {
     TableBuilder<double> tb;
-    rc = mode == TILEFFT_MODE_FAST ? build_fast_1d<double>(P, tb) : build_exact<double>(P, tb, f, tv, tres);
+    rc = mode == TILEFFT_MODE_FAST        ? build_fast_1d<double>(P, tb)
+         : mode == TILEFFT_MODE_LEVELWISE ? build_levelwise<double>(P, tb, tv, tres)
+                                          : build_exact<double>(P, tb, f, tv, tres);
     if (!rc) rc = finish_plan<double>(P, tb);
   }
   if (rc) {
@@ -589,7 +653,7 @@ int tilefft_exec_c2c_host(tilefft_plan_t P, const void* h_in, void* h_out, int s
   const size_t eb = P->elem_bytes;
   const uint64_t B = P->batch;
   // chunked pipeline only for single-pass batched plans whose passes act per transform
-  const bool chunkable = B > 1 && P->passes.size() == 1 && P->passes[0].kind != K_EXACT && !P->is2d;
+  const bool chunkable = B > 1 && P->passes.size() == 1 && P->passes[0].kind == K_ROWS && !P->is2d;
   if (!chunkable) {
     const size_t bytes = per * B * eb;
     if (!P->hbuf[0].p) {
@@ -634,6 +698,61 @@ int tilefft_exec_c2c_host(tilefft_plan_t P, const void* h_in, void* h_out, int s
   }
   for (int i = 0; i < 3; ++i) CUDA_TRY(cudaStreamSynchronize(P->hs[i]));
   return 0;
+}
+
+
+int tilefft_exchange(const void* h_in, void* h_out, uint64_t n, const uint64_t* factors, uint32_t nfactors,
+                     uint32_t stage, uint32_t elem_bytes, int device) {
+  g_err.clear();
+  if (!h_in || !h_out || !factors || nfactors == 0) return fail(TILEFFT_EINVAL, "exchange_transpose: null argument");
+  if (elem_bytes != 8 && elem_bytes != 16) return fail(TILEFFT_EINVAL, "exchange_transpose: elem_bytes must be 8 or 16");
+  if (stage < 1 || stage > nfactors) return fail(TILEFFT_EINVAL, "exchange_transpose: stage out of range");
+  std::vector<uint64_t> f(factors, factors + nfactors);
+  uint64_t prod = 1;
+  for (uint64_t v : f) prod *= v;
+  if (prod != n || nfactors > 64) return fail(TILEFFT_EINVAL, "exchange_transpose: signal length does not match the plan");
+  const Geo g = geometry(n, f);
+  tfb::ExchangeArgs a{};
+  a.n = (long long)n;
+  a.L = (long long)f[stage - 1];
+  a.sub_len = (long long)g.sub_len[stage - 1];
+  a.rps = (long long)g.rps[stage - 1];
+  a.final_pass = stage == nfactors;
+  a.p = (int)nfactors;
+  for (size_t i = 0; i < f.size(); ++i) a.out_w[i] = (long long)g.out_w[i];
+  for (size_t i = 0; i + 1 < f.size(); ++i) a.sub_w[i] = (long long)g.sub_w[i];
+  const size_t bytes = n * elem_bytes;
+  return with_device_buffers(device, h_in, h_out, bytes, bytes, [&](void* din, void* dout) -> int {
+    int rc = elem_bytes == 8 ? launch_exchange<float>(din, dout, a, nullptr) : launch_exchange<double>(din, dout, a, nullptr);
+    if (rc) return rc;
+    CUDA_TRY(cudaDeviceSynchronize());
+    return 0;
+  });
+}
+
+int tilefft_interstage_scale(const void* h_in, void* h_out, uint64_t rows, uint64_t cols, uint64_t row0,
+                             uint64_t rows_per_sub, uint64_t sub_len, const void* table, uint64_t resolution,
+                             uint32_t elem_bytes, int device) {
+  g_err.clear();
+  if (!h_in || !h_out || !table) return fail(TILEFFT_EINVAL, "apply_interstage_twiddles: null argument");
+  if (elem_bytes != 8 && elem_bytes != 16) return fail(TILEFFT_EINVAL, "apply_interstage_twiddles: elem_bytes must be 8 or 16");
+  if (!is_pow2(sub_len) || !is_pow2(resolution) || resolution < sub_len || rows_per_sub == 0)
+    return fail(TILEFFT_EINVAL, "apply_interstage_twiddles: sub-transform length must divide the table resolution");
+  if (int rc = check_device(device)) return rc;
+  DevBuf dt;
+  if (int rc = dt.alloc(resolution * elem_bytes)) return rc;
+  CUDA_TRY(cudaMemcpy(dt.p, table, resolution * elem_bytes, cudaMemcpyHostToDevice));
+  const size_t bytes = rows * cols * elem_bytes;
+  return with_device_buffers(device, h_in, h_out, bytes, bytes, [&](void* din, void* dout) -> int {
+    const long long ts = (long long)(resolution / sub_len);
+    int rc = elem_bytes == 8 ? launch_interstage<float>(din, dout, (long long)rows, (long long)cols, (long long)row0,
+                                                        (long long)rows_per_sub, (long long)sub_len, dt.p, ts, nullptr)
+                             : launch_interstage<double>(din, dout, (long long)rows, (long long)cols, (long long)row0,
+                                                         (long long)rows_per_sub, (long long)sub_len, dt.p, ts, nullptr);
+    if (rc) return rc;
+    CUDA_TRY(cudaDeviceSynchronize());
+    return 0;
+  });
 }
 
 int tilefft_plan_destroy(tilefft_plan_t P) {

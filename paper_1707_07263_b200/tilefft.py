@@ -188,14 +188,13 @@ _cache_lock = threading.Lock()
 
 
 def _device_plan(n, batch, factors, elem_bytes, mode, table, device):
+    uses_table = table is not None and mode in (_capi.MODE_EXACT, _capi.MODE_LEVELWISE)
     key = (n, batch, tuple(factors) if factors else None, elem_bytes, mode,
-           (table.resolution, table.values.ctypes.data) if (table is not None and mode == _capi.MODE_EXACT) else None,
-           device)
+           (table.resolution, table.values.ctypes.data) if uses_table else None, device)
     with _cache_lock:
         p = _plan_cache.get(key)
         if p is None:
-            p = _capi.DevicePlan.create(n, batch, factors, elem_bytes, mode,
-                                        table if mode == _capi.MODE_EXACT else None, device)
+            p = _capi.DevicePlan.create(n, batch, factors, elem_bytes, mode, table if uses_table else None, device)
             _plan_cache[key] = p
         return p
 
@@ -241,6 +240,120 @@ def ifft_tiled(x, plan: StagePlan, table: Optional[TwiddleTable] = None, mode: s
                device: int = 0) -> np.ndarray:
     """tiled_fft.hpp:410-423 (conj -> fft_tiled -> conj * 1/n), on the GPU."""
     return fft_tiled(x, plan, table, mode=mode, device=device, _sign=_capi.INVERSE)
+
+
+# ---- the reference's remaining public ops ----------------------------------------------------------
+def fft_levelwise(x, table: Optional[TwiddleTable] = None, trace=None, device: int = 0,
+                  _sign: int = _capi.FORWARD) -> np.ndarray:
+    """fft_baseline.hpp:66-116 — the paper's previous method on the GPU: a
+    bit-reversal sweep then one launch per radix-2 level in global memory.
+    Bit-identical to the reference's fft_levelwise."""
+    x = np.ascontiguousarray(np.asarray(x))
+    n = x.shape[-1]
+    _require(is_power_of_two(n) and n >= 2, "fft_levelwise: signal length must be a power of two >= 2")
+    if table is not None:
+        _require(table.resolution >= n and table.resolution % n == 0,
+                 "fft_levelwise: signal length must divide the table resolution")
+    batch = int(np.prod(x.shape[:-1])) if x.ndim > 1 else 1
+    dp = _device_plan(n, batch, None, x.dtype.itemsize, _capi.MODE_LEVELWISE, table, device)
+    out = np.empty_like(x)
+    dp.exec_host(x.ctypes.data, out.ctypes.data, _sign)
+    return out
+
+
+def ifft_levelwise(x, table: Optional[TwiddleTable] = None, device: int = 0) -> np.ndarray:
+    """fft_baseline.hpp:120-132."""
+    return fft_levelwise(x, table, device=device, _sign=_capi.INVERSE)
+
+
+def exchange_transpose(data, stage: int, plan: StagePlan, trace=None, device: int = 0) -> np.ndarray:
+    """tiled_fft.hpp:179-203: one sweep applying the pass's store permutation, on the GPU."""
+    data = np.ascontiguousarray(np.asarray(data))
+    _require(1 <= stage <= plan.pass_count(), "exchange_transpose: stage out of range")
+    _require(data.shape[-1] == plan.n_total, "exchange_transpose: signal length does not match the plan")
+    if plan.pass_count() == 1:
+        return data.copy()
+    out = np.empty_like(data)
+    _capi.exchange(data.ctypes.data, out.ctypes.data, plan.n_total, plan.factors, stage, data.dtype.itemsize, device)
+    return out
+
+
+class FastBuffer:
+    """tiled_fft.hpp:38-71 — a rows x cols tile with `stride` slots between rows."""
+
+    def __init__(self, rows, cols, stride, capacity, row_offset=0, dtype=np.complex128):
+        _require(rows >= 1 and cols >= 1, "FastBuffer: empty tile")
+        _require(stride >= cols, "FastBuffer: stride narrower than a row")
+        _require(rows * cols <= capacity, "FastBuffer: tile exceeds capacity")
+        self._rows, self._cols, self._stride, self._capacity = rows, cols, stride, capacity
+        self._row_offset = row_offset
+        self.cells = np.zeros((rows, stride), dtype=dtype)
+
+    def rows(self):
+        return self._rows
+
+    def cols(self):
+        return self._cols
+
+    def stride(self):
+        return self._stride
+
+    def capacity(self):
+        return self._capacity
+
+    def row_offset(self):
+        return self._row_offset
+
+    def set_row_offset(self, v):
+        self._row_offset = v
+
+    def at(self, r, c):
+        return self.cells[r, c]
+
+    def set(self, r, c, v):
+        self.cells[r, c] = v
+
+    def tile(self) -> np.ndarray:
+        return self.cells[:, :self._cols]
+
+
+def make_stage_buffer(plan: StagePlan, stage: int, dtype=np.complex128) -> FastBuffer:  # tiled_fft.hpp:75-80
+    g = plan.stage(stage)
+    return FastBuffer(g.rows_per_tile, g.fft_len, g.padded_stride, plan.tile_capacity, dtype=dtype)
+
+
+def stage_row_fft(buf: FastBuffer, length: int, table: TwiddleTable, device: int = 0) -> None:
+    """tiled_fft.hpp:129-146: in-place transform of each row of the tile, on the
+    GPU (exact tier: bit-identical to the reference's bit-reverse + dit_levels)."""
+    _require(is_power_of_two(length), "stage_row_fft: length must be a power of two")
+    _require(length <= buf.capacity(), "stage_row_fft: length exceeds tile capacity")
+    _require(length == buf.cols(), "stage_row_fft: length must match the tile row width")
+    _require(table.resolution >= length and table.resolution % length == 0,
+             "stage_row_fft: length must divide the table resolution")
+    rows = np.ascontiguousarray(buf.tile()).astype(table.values.dtype)
+    if length == 1:
+        return
+    dp = _device_plan(length, buf.rows(), (length,), rows.dtype.itemsize, _capi.MODE_EXACT, table, device)
+    out = np.empty_like(rows)
+    dp.exec_host(rows.ctypes.data, out.ctypes.data, _capi.FORWARD)
+    buf.cells[:, :length] = out
+
+
+def apply_interstage_twiddles(buf: FastBuffer, stage: int, plan: StagePlan, table: TwiddleTable,
+                              device: int = 0) -> None:
+    """tiled_fft.hpp:153-172, on the GPU (bit-identical)."""
+    _require(plan.pass_count() >= 1, "apply_interstage_twiddles: empty plan")
+    _require(1 <= stage < plan.pass_count(), "apply_interstage_twiddles: stage must be an inter-pass boundary")
+    g = plan.stage(stage)
+    _require(buf.cols() == g.fft_len, "apply_interstage_twiddles: tile width does not match the pass")
+    _require(buf.row_offset() + buf.rows() <= g.rows, "apply_interstage_twiddles: tile rows fall outside the pass grid")
+    _require(table.resolution >= g.sub_len and table.resolution % g.sub_len == 0,
+             "apply_interstage_twiddles: sub-transform length must divide the table resolution")
+    t = np.ascontiguousarray(buf.tile()).astype(table.values.dtype)
+    out = np.empty_like(t)
+    _capi.interstage_scale(t.ctypes.data, out.ctypes.data, buf.rows(), buf.cols(), buf.row_offset(), g.rows_per_sub,
+                           g.sub_len, table.values.ctypes.data, table.resolution, t.dtype.itemsize, device)
+    buf.cells[:, :buf.cols()] = out
 
 
 def fft2_tiled(x, device: int = 0, inverse: bool = False) -> np.ndarray:

@@ -156,3 +156,42 @@ def test_errors_match_reference(tf):
         tf.fft_tiled(x, plan)
     with pytest.raises(ValueError, match="must divide the table resolution"):
         tf.fft_tiled(np.zeros(256, np.complex64), plan, tf.build_twiddle_table(64, np.complex64))
+
+
+@pytest.mark.parametrize("n", [2, 8, 1024, 1 << 16, 1 << 20])
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_levelwise_gpu_bit_identical(tf, oracle, n, dtype):
+    x = oracle.random_bench_signal(n, 1).astype(dtype)
+    got = tf.fft_levelwise(x, tf.build_twiddle_table(n, dtype))
+    assert bits_equal(got, oracle.fft_levelwise(x))
+
+
+def test_levelwise_inverse_roundtrip(tf, oracle):
+    n = 4096
+    x = oracle.random_bench_signal(n, 2)
+    t = tf.build_twiddle_table(n)
+    assert rel_l2(tf.ifft_levelwise(tf.fft_levelwise(x, t), t), x) < 1e-14
+
+
+def test_exchange_transpose_gpu(tf, oracle, reference):
+    for n, cap in [(16, 4), (8, 4), (64, 4), (4096, 64)]:
+        plan = tf.make_plan(n, cap)
+        ramp = np.arange(n, dtype=np.float64).astype(np.complex128)
+        for s in range(1, plan.pass_count() + 1):
+            assert np.array_equal(tf.exchange_transpose(ramp, s, plan), reference.exchange_transpose(ramp, cap, s))
+
+
+def test_stage_row_fft_and_interstage(tf, oracle):
+    table = tf.build_twiddle_table(64)
+    buf = tf.FastBuffer(2, 8, 9, 16)
+    r0, r1 = oracle.random_signal(8, 21), oracle.random_signal(8, 22)
+    buf.cells[0, :8], buf.cells[1, :8] = r0, r1
+    tf.stage_row_fft(buf, 8, table)
+    assert np.max(np.abs(buf.tile()[0] - oracle.dft(r0))) < 1e-12
+    assert np.max(np.abs(buf.tile()[1] - oracle.dft(r1))) < 1e-12
+    plan = tf.make_plan(4, 2)
+    b = tf.make_stage_buffer(plan, 1)
+    b.set_row_offset(1)
+    b.cells[0, :2] = [1.0, 1.0]
+    tf.apply_interstage_twiddles(b, 1, plan, tf.build_twiddle_table(16))
+    assert b.tile()[0, 0] == 1.0 and b.tile()[0, 1] == -1j
