@@ -119,8 +119,8 @@ __global__ void k_bitrev_permute(const C2<Real>* in, C2<Real>* out, long long n,
 }
 
 template <typename Real>
-__global__ void k_level(C2<Real>* w, long long n, int lv, long long total_half, const C2<Real>* __restrict__ tbl,
-                        int conj_scale_out, Real scale) {
+__global__ void k_level(const C2<Real>* w, C2<Real>* o, long long n, int lv, long long total_half,
+                        const C2<Real>* __restrict__ tbl, int conj_scale_out, Real scale) {
   using V = C2<Real>;
   const long long h = 1LL << lv;
   const long long tstride = n / (2 * h);
@@ -138,8 +138,8 @@ __global__ void k_level(C2<Real>* w, long long n, int lv, long long total_half, 
       a = mk(rn_mul(a.x, scale), rn_mul(-a.y, scale));
       c = mk(rn_mul(c.x, scale), rn_mul(-c.y, scale));
     }
-    w[lo] = a;
-    w[hi] = c;
+    o[lo] = a;
+    o[hi] = c;
   }
 }
 

@@ -147,8 +147,8 @@ int launch_levelwise(const Pass& ps, const void* in, void* out, const void* tb, 
                                                                      ps.lw_total, conj_in);
   } else {
     const long long blocks = std::min<long long>((ps.lw_total + threads - 1) / threads, 148LL * 16);
-    tfb::k_level<Real><<<(unsigned)blocks, threads, 0, st>>>((V*)out, ps.lw_n, ps.level, ps.lw_total, (const V*)tb,
-                                                            conj_out, scale);
+    tfb::k_level<Real><<<(unsigned)blocks, threads, 0, st>>>((const V*)in, (V*)out, ps.lw_n, ps.level, ps.lw_total,
+                                                            (const V*)tb, conj_out, scale);
   }
   CUDA_TRY(cudaGetLastError());
   return 0;

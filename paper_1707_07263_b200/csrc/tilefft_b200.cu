@@ -409,7 +409,7 @@ int build_levelwise(tilefft_plan_s* P, TableBuilder<Real>& tb, const void* tv, u
   Pass ps{};
   ps.kind = K_BITREV;
   ps.src = 0;
-  ps.dst = 1;
+  ps.dst = 2;  // workspace: the permutation is not in-place safe (in == out is allowed)
   ps.lw_n = (long long)n;
   ps.lw_total = (long long)(n * P->batch);
   P->passes.push_back(ps);
@@ -417,8 +417,8 @@ int build_levelwise(tilefft_plan_s* P, TableBuilder<Real>& tb, const void* tv, u
   for (int lv = 0; lv < levels; ++lv) {
     Pass q{};
     q.kind = K_LEVEL;
-    q.src = 1;
-    q.dst = 1;
+    q.src = 2;
+    q.dst = lv + 1 == levels ? 1 : 2;
     q.level = lv;
     q.lw_n = (long long)n;
     q.lw_total = (long long)(n / 2 * P->batch);
