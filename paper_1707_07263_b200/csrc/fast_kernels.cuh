@@ -135,12 +135,61 @@ __device__ __forceinline__ int out_index(int t, int j) {
 struct SyncWarp { __device__ __forceinline__ void operator()() const { __syncwarp(); } };
 struct SyncBlock { __device__ __forceinline__ void operator()() const { __syncthreads(); } };
 
-// Inter-pass root W_M^e, e < M, from coarse/fine tables: W = C[e>>B] * F[e & (2^B-1)].
-template <typename V>
-__device__ __forceinline__ V interpass_root(const V* __restrict__ wc, const V* __restrict__ wf, uint32_t e, int fb) {
-  const V c = __ldg(wc + (e >> fb));
-  const V f = __ldg(wf + (e & ((1u << fb) - 1u)));
+// Inter-pass root W_M^e, e < M, from fp64 coarse/fine tables (~sqrt(M)
+// entries each): W = C[e >> fb] * F[e & (2^fb - 1)], product in fp64.
+__device__ __forceinline__ double2 interpass_root64(const double2* __restrict__ wc, const double2* __restrict__ wf,
+                                                    uint32_t e, int fb) {
+  const double2 c = __ldg(wc + (e >> fb));
+  const double2 f = __ldg(wf + (e & ((1u << fb) - 1u)));
   return cmul(c, f);
+}
+__device__ __forceinline__ float2 to_v(double2 w, float2*) { return make_float2((float)w.x, (float)w.y); }
+__device__ __forceinline__ double2 to_v(double2 w, double2*) { return w; }
+
+// Fused inter-pass scale of the last Stockham stage's outputs
+// (tiled_fft.hpp:284-294): register slot i*RS + q holds spectrum index
+// k = b_i + q*(L/RS), b_i = t + T*i, so
+//   W_M^{r k} = W_M^{r b_i} * s^q,   s = W_M^{r L/RS}.
+// Per thread: a handful of fp64 table lookups (two-level, ~sqrt(M) entries)
+// build, in fp64, B_i[qb] = W^{r b_i} s^qb (qb < 4) and A[qa] = s^{4 qa}
+// (qa < RS/4), each rounded once to Real; each element then needs one
+// complex multiply A*B (independent across q: no dependent chain) and the
+// apply — instead of two scattered table gathers per element.
+template <typename V, int L, int RMAX, bool INV>
+__device__ __forceinline__ void interpass_scale(V* v, int t, uint32_t r, uint32_t m_mask, int fb,
+                                                const double2* __restrict__ wc, const double2* __restrict__ wf) {
+  using Sh = Shape<L, RMAX>;
+  constexpr int RSL = Sh::radix(Sh::NST - 1), NB = Sh::R / RSL, STR = L / RSL;
+  constexpr int QB = RSL < 4 ? RSL : 4, QA = RSL / QB;
+  const double2 s1 = interpass_root64(wc, wf, (r * (uint32_t)STR) & m_mask, fb);
+  const double2 s2 = cmul(s1, s1);
+  double2 s4 = cmul(s2, s2);
+  V A[QA];
+  {
+    double2 a = make_double2(1.0, 0.0);
+#pragma unroll
+    for (int qa = 0; qa < QA; ++qa) {
+      A[qa] = to_v(a, (V*)nullptr);
+      if (qa + 1 < QA) a = cmul(a, s4);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const double2 base = interpass_root64(wc, wf, (r * (uint32_t)(t + Sh::T * i)) & m_mask, fb);
+    V B[QB];
+    B[0] = to_v(base, (V*)nullptr);
+    if constexpr (QB > 1) B[1] = to_v(cmul(base, s1), (V*)nullptr);
+    if constexpr (QB > 2) {
+      const double2 b2 = cmul(base, s2);
+      B[2] = to_v(b2, (V*)nullptr);
+      B[3] = to_v(cmul(b2, s1), (V*)nullptr);
+    }
+#pragma unroll
+    for (int q = 0; q < RSL; ++q) {
+      const V w = (q / QB) == 0 ? B[q % QB] : cmul(A[q / QB], B[q % QB]);
+      v[i * RSL + q] = ctw<INV>(v[i * RSL + q], w);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ K_ROWS
@@ -351,12 +400,15 @@ struct CombCfg {
   static constexpr int F = FOf<Real>::v;
   static constexpr int THREADS = F * Sh::T;
   static constexpr int SMEM = (Sh::NST > 1 ? L * F : 1) * (int)sizeof(V);
+  // two resident CTAs per SM (<= 128 registers at 256 threads) so one CTA's
+  // loads overlap the other's butterflies
+  static constexpr int MINB = THREADS <= 256 ? 2 : 1;
 };
 
 template <typename Real, int L, bool INV, bool TWID, int MODE>
-__global__ void __launch_bounds__(CombCfg<Real, L>::THREADS)
+__global__ void __launch_bounds__(CombCfg<Real, L>::THREADS, CombCfg<Real, L>::MINB)
 k_comb(const C2<Real>* in, C2<Real>* out, CombArgs a, const C2<Real>* __restrict__ tw,
-       const C2<Real>* __restrict__ wc, const C2<Real>* __restrict__ wf, Real scale) {
+       const double2* __restrict__ wc, const double2* __restrict__ wf, Real scale) {
   using Cfg = CombCfg<Real, L>;
   using V = C2<Real>;
   using Sh = typename Cfg::Sh;
@@ -397,16 +449,12 @@ k_comb(const C2<Real>* in, C2<Real>* out, CombArgs a, const C2<Real>* __restrict
   auto ex = [sm, f](int i) -> V& { return sm[i * F + f]; };
   SyncBlock s;
   Stages<V, L, Cfg::RMAX, INV, 0>::run(v, t, ex, tw, s);
+  if constexpr (TWID) interpass_scale<V, L, Cfg::RMAX, INV>(v, t, r, a.m_mask, a.fb, wc, wf);
   if (active) {
 #pragma unroll
     for (int j = 0; j < Sh::R; ++j) {
       const int k = out_index<L, Cfg::RMAX>(t, j);
       V x = v[j];
-      if constexpr (TWID) {
-        const uint32_t e = (r * (uint32_t)k) & a.m_mask;
-        const V w = interpass_root(wc, wf, e, a.fb);
-        x = ctw<INV>(x, w);
-      }
       if (scale != (Real)1) x = mk(x.x * scale, x.y * scale);
       out[out_base + f + (long long)k * s_out] = x;
     }
@@ -437,8 +485,11 @@ struct FinalCfg {
   using Sh = Shape<L, RMAX>;
   static constexpr int F = FOf<Real>::v;
   static constexpr int THREADS = F * Sh::T;
-  static constexpr int REG = L + L / 32 + 1;
-  static constexpr int A = F * REG, B = L * (F + 1);
+  // FFT regions == T (mod 16) and a transpose row stride F + 16/T: every
+  // half-warp access (several FFTs per half-warp when T < 16) is conflict free
+  static constexpr int REG = RegionPad<L, Sh::T>::v;
+  static constexpr int TS = F + (Sh::T >= 16 ? 1 : 16 / Sh::T);
+  static constexpr int A = F * REG, B = L * TS;
   static constexpr int SMEM = (A > B ? A : B) * (int)sizeof(V);
 };
 
@@ -472,7 +523,7 @@ k_final_t(const C2<Real>* in, C2<Real>* out, FinalArgs a, const C2<Real>* __rest
     Stages<V, L, Cfg::RMAX, INV, 0>::run(v, t, ex, tw, s);
     __syncthreads();  // exchange regions are reused by the transpose below
 #pragma unroll
-    for (int j = 0; j < Sh::R; ++j) sm[out_index<L, Cfg::RMAX>(t, j) * (F + 1) + ff] = v[j];
+    for (int j = 0; j < Sh::R; ++j) sm[out_index<L, Cfg::RMAX>(t, j) * Cfg::TS + ff] = v[j];
   }
   __syncthreads();
   // phase 2: lanes along the 16 consecutive outputs
@@ -491,7 +542,7 @@ k_final_t(const C2<Real>* in, C2<Real>* out, FinalArgs a, const C2<Real>* __rest
     }();
 #pragma unroll 4
     for (int k = kk; k < L; k += KSTEP) {
-      V x = sm[k * (F + 1) + f];
+      V x = sm[k * Cfg::TS + f];
       if (scale != (Real)1) x = mk(x.x * scale, x.y * scale);
       out[ob + (long long)k * a.out_w_last] = x;
     }

@@ -47,7 +47,8 @@ struct Pass {
 // Kernel launchers, explicitly instantiated in kern_*.cu (one TU per
 // precision/direction so the heavy template instantiation builds in parallel).
 template <typename Real, bool INV>
-int launch_fast(const Pass& ps, const void* in, void* out, const void* tb, Real scale, cudaStream_t st);
+int launch_fast(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, Real scale,
+                cudaStream_t st);
 template <typename Real>
 int launch_exact(const Pass& ps, const void* in, void* out, const void* tb, Real scale, int conj_in, int conj_out,
                  cudaStream_t st);
@@ -61,10 +62,10 @@ template <typename Real>
 int launch_interstage(const void* in, void* out, long long rows, long long cols, long long row0, long long rps,
                       long long sub_len, const void* tbl, long long tstride, cudaStream_t st);
 
-extern template int launch_fast<float, false>(const Pass&, const void*, void*, const void*, float, cudaStream_t);
-extern template int launch_fast<float, true>(const Pass&, const void*, void*, const void*, float, cudaStream_t);
-extern template int launch_fast<double, false>(const Pass&, const void*, void*, const void*, double, cudaStream_t);
-extern template int launch_fast<double, true>(const Pass&, const void*, void*, const void*, double, cudaStream_t);
+extern template int launch_fast<float, false>(const Pass&, const void*, void*, const void*, const void*, float, cudaStream_t);
+extern template int launch_fast<float, true>(const Pass&, const void*, void*, const void*, const void*, float, cudaStream_t);
+extern template int launch_fast<double, false>(const Pass&, const void*, void*, const void*, const void*, double, cudaStream_t);
+extern template int launch_fast<double, true>(const Pass&, const void*, void*, const void*, const void*, double, cudaStream_t);
 extern template int launch_exact<float>(const Pass&, const void*, void*, const void*, float, int, int, cudaStream_t);
 extern template int launch_levelwise<float>(const Pass&, const void*, void*, const void*, float, int, int,
                                            cudaStream_t);

@@ -2,5 +2,5 @@
 #include "launch.cuh"
 
 namespace tfb_host {
-template int launch_fast<double, true>(const Pass&, const void*, void*, const void*, double, cudaStream_t);
+template int launch_fast<double, true>(const Pass&, const void*, void*, const void*, const void*, double, cudaStream_t);
 }  // namespace tfb_host

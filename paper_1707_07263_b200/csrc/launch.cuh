@@ -21,7 +21,7 @@ constexpr int kRowsWarps = 4;
 constexpr int kRowsStages = 2;
 
 template <typename Real, int L, bool INV>
-int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, Real scale, cudaStream_t st) {
+int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, const void*, Real scale, cudaStream_t st) {
   constexpr int RM = tfb::RmaxOf<Real>::v;
   constexpr int T = (L < RM ? 1 : L / RM);
   const bool aligned = ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0) && (L * sizeof(tfb::C2<Real>)) % 16 == 0;
@@ -61,14 +61,16 @@ int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, Real 
 }
 
 template <typename Real, int L, bool INV>
-int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, Real scale, cudaStream_t st) {
+int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, Real scale,
+                cudaStream_t st) {
   using Cfg = tfb::CombCfg<Real, L>;
   using V = tfb::C2<Real>;
   const V* t = (const V*)tb;
   auto go = [&](auto k) -> int {
     if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
+    const double2* t64 = (const double2*)tb64;
     k<<<(unsigned)ps.grid, Cfg::THREADS, Cfg::SMEM, st>>>((const V*)in, (V*)out, ps.comb, t + ps.tw_off,
-                                                          t + ps.wc_off, t + ps.wf_off, scale);
+                                                          t64 + ps.wc_off, t64 + ps.wf_off, scale);
     CUDA_TRY(cudaGetLastError());
     return 0;
   };
@@ -78,7 +80,8 @@ int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, Real 
 }
 
 template <typename Real, int L, bool INV>
-int launch_final(const Pass& ps, const void* in, void* out, const void* tb, Real scale, cudaStream_t st) {
+int launch_final(const Pass& ps, const void* in, void* out, const void* tb, const void*, Real scale,
+                 cudaStream_t st) {
   using Cfg = tfb::FinalCfg<Real, L>;
   using V = tfb::C2<Real>;
   auto k = tfb::k_final_t<Real, L, INV>;
@@ -90,26 +93,27 @@ int launch_final(const Pass& ps, const void* in, void* out, const void* tb, Real
 }
 
 template <typename Real, bool INV>
-int launch_fast(const Pass& ps, const void* in, void* out, const void* tb, Real scale, cudaStream_t st) {
+int launch_fast(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, Real scale,
+                cudaStream_t st) {
 #define DISPATCH(FN, ...)                                                     \
   switch (ps.L) {                                                             \
-    case 2: return FN<Real, 2, INV>(ps, in, out, tb, scale, st);              \
-    case 4: return FN<Real, 4, INV>(ps, in, out, tb, scale, st);              \
-    case 8: return FN<Real, 8, INV>(ps, in, out, tb, scale, st);              \
-    case 16: return FN<Real, 16, INV>(ps, in, out, tb, scale, st);            \
-    case 32: return FN<Real, 32, INV>(ps, in, out, tb, scale, st);            \
-    case 64: return FN<Real, 64, INV>(ps, in, out, tb, scale, st);            \
-    case 128: return FN<Real, 128, INV>(ps, in, out, tb, scale, st);          \
-    case 256: return FN<Real, 256, INV>(ps, in, out, tb, scale, st);          \
-    case 512: return FN<Real, 512, INV>(ps, in, out, tb, scale, st);          \
-    case 1024: return FN<Real, 1024, INV>(ps, in, out, tb, scale, st);        \
+    case 2: return FN<Real, 2, INV>(ps, in, out, tb, tb64, scale, st);              \
+    case 4: return FN<Real, 4, INV>(ps, in, out, tb, tb64, scale, st);              \
+    case 8: return FN<Real, 8, INV>(ps, in, out, tb, tb64, scale, st);              \
+    case 16: return FN<Real, 16, INV>(ps, in, out, tb, tb64, scale, st);            \
+    case 32: return FN<Real, 32, INV>(ps, in, out, tb, tb64, scale, st);            \
+    case 64: return FN<Real, 64, INV>(ps, in, out, tb, tb64, scale, st);            \
+    case 128: return FN<Real, 128, INV>(ps, in, out, tb, tb64, scale, st);          \
+    case 256: return FN<Real, 256, INV>(ps, in, out, tb, tb64, scale, st);          \
+    case 512: return FN<Real, 512, INV>(ps, in, out, tb, tb64, scale, st);          \
+    case 1024: return FN<Real, 1024, INV>(ps, in, out, tb, tb64, scale, st);        \
     __VA_ARGS__                                                               \
   }
   if (ps.kind == K_ROWS) {
     DISPATCH(launch_rows,
-             case 2048: return launch_rows<Real, 2048, INV>(ps, in, out, tb, scale, st);
-             case 4096: return launch_rows<Real, 4096, INV>(ps, in, out, tb, scale, st);
-             case 8192: return launch_rows<Real, 8192, INV>(ps, in, out, tb, scale, st);)
+             case 2048: return launch_rows<Real, 2048, INV>(ps, in, out, tb, tb64, scale, st);
+             case 4096: return launch_rows<Real, 4096, INV>(ps, in, out, tb, tb64, scale, st);
+             case 8192: return launch_rows<Real, 8192, INV>(ps, in, out, tb, tb64, scale, st);)
   } else if (ps.kind == K_COMB1D || ps.kind == K_COMBAX) {
     DISPATCH(launch_comb)
   } else if (ps.kind == K_FINALT) {

@@ -106,6 +106,19 @@ struct DevBuf {
 
 }  // namespace
 
+namespace {
+template <typename Real>
+struct TableBuilder {
+  std::vector<Real> h;  // interleaved
+  size_t add(size_t count) {
+    size_t off = h.size() / 2;
+    h.resize(h.size() + 2 * count);
+    return off;
+  }
+  void set(size_t idx, Real re, Real im) { h[2 * idx] = re; h[2 * idx + 1] = im; }
+};
+}  // namespace
+
 struct tilefft_plan_s {
   int device = 0;
   uint64_t n = 0, batch = 0, ny = 0, nx = 0;
@@ -113,6 +126,8 @@ struct tilefft_plan_s {
   std::vector<uint64_t> dev_factors;
   std::vector<Pass> passes;
   DevBuf tables;          // all device tables (elements of C2<Real>)
+  DevBuf tables64;        // fp64 inter-pass root tables
+  TableBuilder<double>* tb64 = nullptr;  // plan-build scratch
   DevBuf work;            // workspace (batch * n elements)
   size_t table_elems = 0;
   // host-path staging
@@ -132,16 +147,6 @@ struct tilefft_plan_s {
 namespace {
 
 // ---------------------------------------------------------------- table builder
-template <typename Real>
-struct TableBuilder {
-  std::vector<Real> h;  // interleaved
-  size_t add(size_t count) {
-    size_t off = h.size() / 2;
-    h.resize(h.size() + 2 * count);
-    return off;
-  }
-  void set(size_t idx, Real re, Real im) { h[2 * idx] = re; h[2 * idx + 1] = im; }
-};
 
 template <typename Real>
 tfb::StageTableInfo stage_info_for(int L) {
@@ -174,22 +179,22 @@ size_t add_stage_table(TableBuilder<Real>& tb, int L) {
   return off;
 }
 
-// Inter-pass roots W_M^e = C[e >> fb] * F[e & (2^fb - 1)].
-template <typename Real>
-void add_interpass(TableBuilder<Real>& tb, uint64_t M, size_t* wc, size_t* wf, int* fb) {
+// Inter-pass roots W_M^e = C[e >> fb] * F[e & (2^fb - 1)], fp64 for both
+// precisions (the kernels walk powers from them in fp64).
+void add_interpass(TableBuilder<double>& tb, uint64_t M, size_t* wc, size_t* wf, int* fb) {
   const int lm = ilog2(M);
   *fb = (lm + 1) / 2;
   const uint64_t nf = 1ull << *fb, nc = M >> *fb;
   *wc = tb.add(nc);
   for (uint64_t i = 0; i < nc; ++i) {
-    Real re, im;
-    acc_root<Real>(i * nf, M, &re, &im);
+    double re, im;
+    acc_root<double>(i * nf, M, &re, &im);
     tb.set(*wc + i, re, im);
   }
   *wf = tb.add(nf);
   for (uint64_t j = 0; j < nf; ++j) {
-    Real re, im;
-    acc_root<Real>(j, M, &re, &im);
+    double re, im;
+    acc_root<double>(j, M, &re, &im);
     tb.set(*wf + j, re, im);
   }
 }
@@ -254,7 +259,7 @@ int build_fast_1d(tilefft_plan_s* P, TableBuilder<Real>& tb) {
       ps.dst = 2;
       ps.twid = true;
       int fb;
-      add_interpass(tb, g.sub_len[s], &ps.wc_off, &ps.wf_off, &fb);
+      add_interpass(*P->tb64, g.sub_len[s], &ps.wc_off, &ps.wf_off, &fb);
       tfb::CombArgs& a = ps.comb;
       a.bstride = (long long)n;
       a.chunks = (long long)(g.rps[s] / kF);
@@ -312,7 +317,7 @@ int build_axis_passes(tilefft_plan_s* P, TableBuilder<Real>& tb, uint64_t ny, ui
     ps.final_pass = s + 1 == p;
     tfb::CombArgs& a = ps.comb;
     int fb = 0;
-    if (ps.twid) add_interpass(tb, g.sub_len[s], &ps.wc_off, &ps.wf_off, &fb);
+    if (ps.twid) add_interpass(*P->tb64, g.sub_len[s], &ps.wc_off, &ps.wf_off, &fb);
     a.bstride = (long long)(ny * nx);
     a.chunks = (long long)((nx + kF - 1) / kF);
     a.fvalid = (int)std::min<uint64_t>(kF, nx);
@@ -454,6 +459,11 @@ int finish_plan(tilefft_plan_s* P, TableBuilder<Real>& tb) {
     int rc = P->work.alloc(elems * sizeof(tfb::C2<Real>));
     if (rc) return rc;
   }
+  if (P->tb64 && !P->tb64->h.empty()) {
+    int rc = P->tables64.alloc(P->tb64->h.size() * sizeof(double));
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpy(P->tables64.p, P->tb64->h.data(), P->tb64->h.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
   P->table_elems = tb.h.size() / 2;
   if (P->table_elems) {
     int rc = P->tables.alloc(tb.h.size() * sizeof(Real));
@@ -480,9 +490,9 @@ int exec_impl(tilefft_plan_s* P, const void* in, void* out, int sign, cudaStream
       rc = launch_levelwise<Real>(ps, src, dst, P->tables.p, scale, inv && ps.kind == K_BITREV,
                                   inv && ps.final_pass, st);
     } else if (inv) {
-      rc = launch_fast<Real, true>(ps, src, dst, P->tables.p, ps.final_pass ? scale : (Real)1, st);
+      rc = launch_fast<Real, true>(ps, src, dst, P->tables.p, P->tables64.p, ps.final_pass ? scale : (Real)1, st);
     } else {
-      rc = launch_fast<Real, false>(ps, src, dst, P->tables.p, (Real)1, st);
+      rc = launch_fast<Real, false>(ps, src, dst, P->tables.p, P->tables64.p, (Real)1, st);
     }
     if (rc) return rc;
   }
@@ -563,6 +573,8 @@ int tilefft_plan_create(tilefft_plan_t* out, uint64_t n, uint64_t batch, const u
   P->elem_bytes = elem_bytes;
   P->mode = mode;
   int rc;
+  TableBuilder<double> tb64;
+  P->tb64 = &tb64;
   if (elem_bytes == 8) {
     TableBuilder<float> tb;
     rc = mode == TILEFFT_MODE_FAST        ? build_fast_1d<float>(P, tb)
@@ -576,6 +588,7 @@ int tilefft_plan_create(tilefft_plan_t* out, uint64_t n, uint64_t batch, const u
                                           : build_exact<double>(P, tb, f, tv, tres);
     if (!rc) rc = finish_plan<double>(P, tb);
   }
+  P->tb64 = nullptr;
   if (rc) {
     delete P;
     return rc;
@@ -605,6 +618,8 @@ int tilefft_plan_create_2d(tilefft_plan_t* out, uint64_t ny, uint64_t nx, uint64
   P->batch = batch;
   P->elem_bytes = elem_bytes;
   P->mode = TILEFFT_MODE_FAST;
+  TableBuilder<double> tb64;
+  P->tb64 = &tb64;
   auto build = [&](auto tbv) -> int {
     using Real = std::remove_reference_t<decltype(tbv.h[0])>;
     TableBuilder<Real> tb;
@@ -623,6 +638,7 @@ int tilefft_plan_create_2d(tilefft_plan_t* out, uint64_t ny, uint64_t nx, uint64
     return finish_plan<Real>(P, tb);
   };
   int rc = elem_bytes == 8 ? build(TableBuilder<float>{}) : build(TableBuilder<double>{});
+  P->tb64 = nullptr;
   if (rc) {
     delete P;
     return rc;
@@ -686,12 +702,12 @@ int tilefft_exec_c2c_host(tilefft_plan_t P, const void* h_in, void* h_out, int s
     int rc;
     if (P->elem_bytes == 8) {
       const float scale = inv ? 1.0f / (float)per : 1.0f;
-      rc = inv ? launch_fast<float, true>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, scale, st)
-               : launch_fast<float, false>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, scale, st);
+      rc = inv ? launch_fast<float, true>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, nullptr, scale, st)
+               : launch_fast<float, false>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, nullptr, scale, st);
     } else {
       const double scale = inv ? 1.0 / (double)per : 1.0;
-      rc = inv ? launch_fast<double, true>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, scale, st)
-               : launch_fast<double, false>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, scale, st);
+      rc = inv ? launch_fast<double, true>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, nullptr, scale, st)
+               : launch_fast<double, false>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, nullptr, scale, st);
     }
     if (rc) return rc;
     CUDA_TRY(cudaMemcpyAsync((char*)h_out + off, P->hbuf[ci].p, bytes, cudaMemcpyDeviceToHost, st));
