@@ -23,6 +23,7 @@
 #pragma once
 #include "fft_common.cuh"
 #include "tma_util.cuh"
+#include <cuda.h>
 
 namespace tfb {
 
@@ -84,12 +85,15 @@ __device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
 // ------------------------------------------------------------------ Stockham
 // v[i*RS + q]: input q of butterfly b = t + T*i of the current stage.
 // After the last stage v[i*RS + q] = X[b + q * (L / RS_last)].
-template <typename V, int L, int RMAX, bool INV, int S>
+template <typename V, int L, int RMAX, bool INV, int S, int NR = 1>
 struct Stages {
   using Sh = Shape<L, RMAX>;
   static constexpr int RS = Sh::radix(S), NS = Sh::ns(S), NB = Sh::R / RS;
+  // NR > 1: the exchange buffer holds 1/NR of the CTA's FFTs; the exchange
+  // runs in NR rounds and a thread takes part in round `my_round` only.
   template <class Ex, class Sync>
-  __device__ __forceinline__ static void run(V* v, int t, Ex& ex, const V* __restrict__ tw, Sync& sync) {
+  __device__ __forceinline__ static void run(V* v, int t, Ex& ex, const V* __restrict__ tw, Sync& sync,
+                                             int my_round = 0) {
     if constexpr (S > 0) {
       const V* tws = tw + Sh::tw_off(S);
 #pragma unroll
@@ -102,23 +106,30 @@ struct Stages {
 #pragma unroll
     for (int i = 0; i < NB; ++i) reg_dft<RS, INV>(v + i * RS);
     if constexpr (S + 1 < Sh::NST) {
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        const int b = t + Sh::T * i;
-        const int base = (b / NS) * (NS * RS) + (b & (NS - 1));
-#pragma unroll
-        for (int q = 0; q < RS; ++q) ex(base + q * NS) = v[i * RS + q];
-      }
-      sync();
       constexpr int RS2 = Sh::radix(S + 1), NB2 = Sh::R / RS2, STR2 = L / RS2;
+#pragma unroll 1
+      for (int round = 0; round < NR; ++round) {
+        if (round == my_round) {
 #pragma unroll
-      for (int i = 0; i < NB2; ++i) {
-        const int b = t + Sh::T * i;
+          for (int i = 0; i < NB; ++i) {
+            const int b = t + Sh::T * i;
+            const int base = (b / NS) * (NS * RS) + (b & (NS - 1));
 #pragma unroll
-        for (int q = 0; q < RS2; ++q) v[i * RS2 + q] = ex(b + q * STR2);
+            for (int q = 0; q < RS; ++q) ex(base + q * NS) = v[i * RS + q];
+          }
+        }
+        sync();
+        if (round == my_round) {
+#pragma unroll
+          for (int i = 0; i < NB2; ++i) {
+            const int b = t + Sh::T * i;
+#pragma unroll
+            for (int q = 0; q < RS2; ++q) v[i * RS2 + q] = ex(b + q * STR2);
+          }
+        }
+        sync();
       }
-      sync();
-      Stages<V, L, RMAX, INV, S + 1>::run(v, t, ex, tw, sync);
+      Stages<V, L, RMAX, INV, S + 1, NR>::run(v, t, ex, tw, sync, my_round);
     }
   }
 };
@@ -457,6 +468,160 @@ k_comb(const C2<Real>* in, C2<Real>* out, CombArgs a, const C2<Real>* __restrict
       V x = v[j];
       if (scale != (Real)1) x = mk(x.x * scale, x.y * scale);
       out[out_base + f + (long long)k * s_out] = x;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K_COMB_TMA
+// Persistent, TMA-pipelined K_COMB. Tiles are [L][F] boxes of 16 adjacent
+// combs (fp32; 8 for fp64): one 128-byte line per comb step. A 3-D/4-D
+// tensor map describes the strided comb layout, so one thread streams whole
+// tiles into an S-deep ring of shared-memory slots (cp.async.bulk.tensor +
+// mbarrier complete_tx) while the CTA works on the current tile; the slot is
+// released as soon as its inputs are in registers, so the next tile's load
+// overlaps the butterflies, the exchange (a separate buffer, in NR rounds
+// when the tile is larger than it) and the stores.
+template <typename Real, int L>
+struct CombTmaCfg {
+  using V = C2<Real>;
+  static constexpr int RMAX = RmaxOf<Real>::v;
+  using Sh = Shape<L, RMAX>;
+  static constexpr int F = FOf<Real>::v;
+  static constexpr int THREADS = F * Sh::T;
+  static constexpr int TILE = L * F;                       // elements
+  static constexpr int TILE_BYTES = TILE * (int)sizeof(V);
+  // One slot per CTA (released as soon as the tile is in registers, so the
+  // next tile streams in during the butterflies) plus a half-tile exchange
+  // buffer used in two rounds: 1.5 tiles of shared memory, which lets >= 16
+  // warps per SM stay resident (2 CTAs of 8 warps at L = 512, ...).
+  static constexpr int S = 1;
+  static constexpr int NR = Sh::NST > 1 ? 2 : 1;
+  static constexpr int FX = F / NR;                        // FFTs per exchange round
+  static constexpr int XB = Sh::NST > 1 ? L * FX : 0;      // exchange elements
+  static constexpr int BL = L < 256 ? L : 256;             // TMA box rows
+  static constexpr int DATA_BYTES = S * TILE_BYTES + XB * (int)sizeof(V);
+  static constexpr int SMEM = DATA_BYTES + S * 8 + 128;    // + mbarriers + alignment slack
+  static constexpr int WARPS = THREADS / 32 > 0 ? THREADS / 32 : 1;
+  static constexpr int MINB_W = 16 / WARPS > 0 ? 16 / WARPS : 1;
+  static constexpr int MINB_S = (227 * 1024) / (SMEM + 1024) > 0 ? (227 * 1024) / (SMEM + 1024) : 1;
+  static constexpr int MINB = MINB_W < MINB_S ? MINB_W : MINB_S;
+};
+
+struct CombTmaArgs {
+  long long ntiles, chunks, groups_per_batch;
+  long long rps, sub_len;   // pass geometry (logical units)
+  long long es;             // element stride (mode 1)
+  long long bstride;        // elements between batch items
+  long long out_w_last;     // final pass of mode 1
+  int final_pass, fvalid, fb, p;
+  uint32_t m_mask;
+  long long out_w[8], sub_w[8];
+};
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename Real, int L, bool INV, bool TWID, int MODE>
+__global__ void __launch_bounds__(CombTmaCfg<Real, L>::THREADS, CombTmaCfg<Real, L>::MINB)
+k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs a, const C2<Real>* __restrict__ tw,
+           const double2* __restrict__ wc, const double2* __restrict__ wf, Real scale) {
+  using Cfg = CombTmaCfg<Real, L>;
+  using V = C2<Real>;
+  using Sh = typename Cfg::Sh;
+  constexpr int F = Cfg::F, S = Cfg::S;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  V* slots = reinterpret_cast<V*>(smem_raw);
+  V* xb = slots + S * Cfg::TILE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + Cfg::DATA_BYTES);
+  const int f = threadIdx.x % F, t = threadIdx.x / F;
+  const int my_round = f / Cfg::FX, fx = f % Cfg::FX;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  // tile -> TMA coordinates {col, n0, rr, group}
+  auto coords = [&](long long tile, int& c0, int& c2, int& c3) {
+    const long long chunk = tile % a.chunks, g = tile / a.chunks;
+    const long long batch = g / a.groups_per_batch, u = g % a.groups_per_batch;
+    c0 = (int)(chunk * F * (sizeof(V) / 8));
+    if constexpr (MODE == 0) {
+      c2 = 0;
+      c3 = (int)(batch * a.groups_per_batch + u);
+    } else {
+      c2 = (int)(u % a.rps);
+      c3 = (int)(batch * (a.groups_per_batch / a.rps) + u / a.rps);
+    }
+  };
+  auto issue = [&](long long tile, int s) {
+    int c0, c2, c3;
+    coords(tile, c0, c2, c3);
+    mbar_arrive_expect_tx(&full[s], Cfg::TILE_BYTES);
+#pragma unroll 1
+    for (int n0 = 0; n0 < L; n0 += Cfg::BL) tma_load_4d(slots + s * Cfg::TILE + n0 * F, &tmap, c0, n0, c2, c3, &full[s]);
+  };
+  const long long G = gridDim.x;
+  long long tile = blockIdx.x;
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int s = 0; s < S; ++s)
+      if (tile + s * G < a.ntiles) issue(tile + s * G, s);
+  }
+  int k = 0;
+#pragma unroll 1
+  for (; tile < a.ntiles; tile += G, ++k) {
+    const int s = k % S;
+    mbar_wait(&full[s], (uint32_t)((k / S) & 1));
+    const V* sl = slots + s * Cfg::TILE;
+    V v[Sh::R];
+#pragma unroll
+    for (int q = 0; q < Sh::R; ++q) v[q] = sl[(t + q * Sh::T) * F + f];
+    fence_proxy_async_smem();
+    __syncthreads();  // slot s fully consumed: refill it
+    if (threadIdx.x == 0 && tile + S * G < a.ntiles) issue(tile + S * G, s);
+    // geometry of this tile (same decomposition as K_COMB)
+    const long long chunk = tile % a.chunks, g = tile / a.chunks;
+    const long long batch = g / a.groups_per_batch, u = g % a.groups_per_batch;
+    long long out_base, s_out;
+    uint32_t r;
+    if constexpr (MODE == 0) {
+      out_base = batch * a.bstride + u * a.sub_len + chunk * F;
+      s_out = a.rps;
+      r = (uint32_t)(chunk * F + f);
+    } else {
+      const long long sub = u / a.rps, rr = u % a.rps;
+      r = (uint32_t)rr;
+      if (a.final_pass) {
+        long long oi = 0, rem = u;
+        for (int i = 0; i + 1 < a.p; ++i) {
+          const long long d = rem / a.sub_w[i];
+          rem -= d * a.sub_w[i];
+          oi += d * a.out_w[i];
+        }
+        out_base = batch * a.bstride + oi * a.es + chunk * F;
+        s_out = a.out_w_last * a.es;
+      } else {
+        out_base = batch * a.bstride + (sub * a.sub_len + rr) * a.es + chunk * F;
+        s_out = a.rps * a.es;
+      }
+    }
+    auto ex = [xb, fx](int i) -> V& { return xb[i * Cfg::FX + fx]; };
+    SyncBlock sy;
+    Stages<V, L, Cfg::RMAX, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
+    if constexpr (TWID) interpass_scale<V, L, Cfg::RMAX, INV>(v, t, r, a.m_mask, a.fb, wc, wf);
+    if (f < a.fvalid) {
+#pragma unroll
+      for (int j = 0; j < Sh::R; ++j) {
+        const int kk = out_index<L, Cfg::RMAX>(t, j);
+        V x = v[j];
+        if (scale != (Real)1) x = mk(x.x * scale, x.y * scale);
+        out[out_base + f + (long long)kk * s_out] = x;
+      }
     }
   }
 }
