@@ -114,6 +114,33 @@ TILEFFT_API int tilefft_interstage_scale(const void* h_in, void* h_out, uint64_t
                                          uint64_t rows_per_sub, uint64_t sub_len, const void* table,
                                          uint64_t resolution, uint32_t elem_bytes, int device);
 
+/* ---- Distributed four-step transform -------------------------
+ * One length-n transform over `nranks` GPUs (one process per GPU), n = N1 x N2
+ * with N1 <= 1024. Layouts (rank g, C = N2/nranks, R = N1/nranks):
+ *   input  column slab  [N1][C]  : x[g*C + c + N2*n1]
+ *   output row slab     [R][N2]  : X[(g*R + k1) + N1*k2]  (digit-interleaved)
+ * Pass 1 (column FFTs + inter-pass root W_N^{r k1}) scatters every result
+ * straight into the destination slabs set by tilefft_dist_set_peers: the
+ * other ranks' row slabs mapped over NVLink (CUDA IPC; row_pitch = N2,
+ * col_off = g*C) — the all-to-all fused into the pass-1 store — or local
+ * staging blocks (row_pitch = C, col_off = 0) for an NCCL all-to-all.
+ * Pass 2 runs the row FFTs of length N2 on the rank's assembled row slab. The
+ * caller orders pass 1 on every rank before pass 2 (stream sync + barrier). */
+TILEFFT_API int tilefft_dist_plan_create(tilefft_plan_t* plan, uint64_t n, uint32_t nranks, uint32_t rank,
+                                         uint32_t elem_bytes, int device);
+TILEFFT_API int tilefft_dist_layout(tilefft_plan_t plan, uint64_t* n1, uint64_t* n2, uint64_t* cols_per_rank,
+                                    uint64_t* rows_per_rank);
+TILEFFT_API int tilefft_dist_set_peers(tilefft_plan_t plan, void* const* dest, uint32_t ndest, uint64_t row_pitch,
+                                       uint64_t col_off);
+TILEFFT_API int tilefft_dist_exec_pass1(tilefft_plan_t plan, const void* d_col_slab, int sign, void* cuda_stream);
+TILEFFT_API int tilefft_dist_exec_pass2(tilefft_plan_t plan, const void* d_row_slab, void* d_out, int sign,
+                                        void* cuda_stream);
+/* CUDA IPC helpers for exchanging slab pointers between rank processes
+ * (handle = 64 opaque bytes). */
+TILEFFT_API int tilefft_ipc_get_handle(const void* dptr, void* handle_out);
+TILEFFT_API int tilefft_ipc_open_handle(const void* handle, void** dptr);
+TILEFFT_API int tilefft_ipc_close_handle(void* dptr);
+
 /* Host-side root table with the reference's construction: entry j =
  * exp(-2 pi i j / resolution), interleaved, elem_bytes 8 or 16
  * (build_twiddle_table, twiddle.hpp:47-73; bit-identical values). */

@@ -57,6 +57,14 @@ EXPORTS = (
     "tilefft_build_twiddle",
     "tilefft_exchange",
     "tilefft_interstage_scale",
+    "tilefft_dist_plan_create",
+    "tilefft_dist_layout",
+    "tilefft_dist_set_peers",
+    "tilefft_dist_exec_pass1",
+    "tilefft_dist_exec_pass2",
+    "tilefft_ipc_get_handle",
+    "tilefft_ipc_open_handle",
+    "tilefft_ipc_close_handle",
     "tilefft_last_error",
     "tilefft_version",
 )
@@ -94,11 +102,21 @@ def load() -> ctypes.CDLL:
         lib.tilefft_build_twiddle.argtypes = [u64, u32, vp]
         lib.tilefft_exchange.argtypes = [vp, vp, u64, ctypes.POINTER(u64), u32, u32, u32, i32]
         lib.tilefft_interstage_scale.argtypes = [vp, vp, u64, u64, u64, u64, u64, vp, u64, u32, i32]
+        lib.tilefft_dist_plan_create.argtypes = [ctypes.POINTER(vp), u64, u32, u32, u32, i32]
+        lib.tilefft_dist_layout.argtypes = [vp] + [ctypes.POINTER(u64)] * 4
+        lib.tilefft_dist_set_peers.argtypes = [vp, ctypes.POINTER(vp), u32, u64, u64]
+        lib.tilefft_dist_exec_pass1.argtypes = [vp, vp, i32, vp]
+        lib.tilefft_dist_exec_pass2.argtypes = [vp, vp, vp, i32, vp]
+        lib.tilefft_ipc_get_handle.argtypes = [vp, vp]
+        lib.tilefft_ipc_open_handle.argtypes = [vp, ctypes.POINTER(vp)]
+        lib.tilefft_ipc_close_handle.argtypes = [vp]
         lib.tilefft_last_error.restype = ctypes.c_char_p
         lib.tilefft_version.restype = ctypes.c_char_p
         for name in ("tilefft_plan_create", "tilefft_plan_create_2d", "tilefft_exec_c2c", "tilefft_exec_c2c_host",
                      "tilefft_plan_destroy", "tilefft_plan_info", "tilefft_build_twiddle", "tilefft_exchange",
-                     "tilefft_interstage_scale"):
+                     "tilefft_interstage_scale", "tilefft_dist_plan_create", "tilefft_dist_layout",
+                     "tilefft_dist_set_peers", "tilefft_dist_exec_pass1", "tilefft_dist_exec_pass2",
+                     "tilefft_ipc_get_handle", "tilefft_ipc_open_handle", "tilefft_ipc_close_handle"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
         return lib
@@ -185,3 +203,48 @@ def interstage_scale(h_in: int, h_out: int, rows: int, cols: int, row0: int, row
 
 def build_twiddle(resolution: int, elem_bytes: int, out_ptr: int) -> None:
     check(load().tilefft_build_twiddle(int(resolution), int(elem_bytes), ctypes.c_void_p(out_ptr)))
+
+
+class DistPlan(DevicePlan):
+    """One rank's share of a distributed four-step transform (tilefft_dist_*)."""
+
+    @classmethod
+    def create_dist(cls, n, nranks, rank, elem_bytes=8, device=0):
+        lib = load()
+        h = ctypes.c_void_p()
+        check(lib.tilefft_dist_plan_create(ctypes.byref(h), int(n), int(nranks), int(rank), int(elem_bytes),
+                                           int(device)))
+        return cls(h.value, lib)
+
+    def layout(self):
+        v = [ctypes.c_uint64() for _ in range(4)]
+        check(self._lib.tilefft_dist_layout(self._h, *[ctypes.byref(x) for x in v]))
+        return dict(n1=v[0].value, n2=v[1].value, cols_per_rank=v[2].value, rows_per_rank=v[3].value)
+
+    def set_peers(self, ptrs, row_pitch, col_off):
+        arr = (ctypes.c_void_p * len(ptrs))(*[int(p) for p in ptrs])
+        check(self._lib.tilefft_dist_set_peers(self._h, arr, len(ptrs), int(row_pitch), int(col_off)))
+
+    def pass1(self, d_slab, sign=FORWARD, stream=0):
+        check(self._lib.tilefft_dist_exec_pass1(self._h, ctypes.c_void_p(d_slab), int(sign), ctypes.c_void_p(stream)))
+
+    def pass2(self, d_rows, d_out, sign=FORWARD, stream=0):
+        check(self._lib.tilefft_dist_exec_pass2(self._h, ctypes.c_void_p(d_rows), ctypes.c_void_p(d_out), int(sign),
+                                                ctypes.c_void_p(stream)))
+
+
+def ipc_handle(dptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    check(load().tilefft_ipc_get_handle(ctypes.c_void_p(dptr), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(bytes(handle), 64)
+    check(load().tilefft_ipc_open_handle(buf, ctypes.byref(p)))
+    return p.value
+
+
+def ipc_close(dptr: int) -> None:
+    check(load().tilefft_ipc_close_handle(ctypes.c_void_p(dptr)))

@@ -516,6 +516,13 @@ struct CombTmaArgs {
   int final_pass, fvalid, fb, p;
   uint32_t m_mask;
   long long out_w[8], sub_w[8];
+  // mode 2 (distributed four-step, pass 1): the CTA's combs are the global
+  // columns r_off + chunk*F + f; spectrum k goes to rank k / rows_per_rank,
+  // row k % rows_per_rank of that rank's slab (row pitch `pitch`, column
+  // offset `col_off`) — the all-to-all transpose fused into the store.
+  long long r_off, pitch, col_off;
+  int rows_per_rank, nranks;
+  void* peers[16];
 };
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
@@ -550,7 +557,7 @@ k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs 
     const long long chunk = tile % a.chunks, g = tile / a.chunks;
     const long long batch = g / a.groups_per_batch, u = g % a.groups_per_batch;
     c0 = (int)(chunk * F * (sizeof(V) / 8));
-    if constexpr (MODE == 0) {
+    if constexpr (MODE == 0 || MODE == 2) {
       c2 = 0;
       c3 = (int)(batch * a.groups_per_batch + u);
     } else {
@@ -593,6 +600,10 @@ k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs 
       out_base = batch * a.bstride + u * a.sub_len + chunk * F;
       s_out = a.rps;
       r = (uint32_t)(chunk * F + f);
+    } else if constexpr (MODE == 2) {
+      out_base = a.col_off + chunk * F;
+      s_out = a.pitch;
+      r = (uint32_t)(a.r_off + chunk * F + f);
     } else {
       const long long sub = u / a.rps, rr = u % a.rps;
       r = (uint32_t)rr;
@@ -620,7 +631,13 @@ k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs 
         const int kk = out_index<L, Cfg::RMAX>(t, j);
         V x = v[j];
         if (scale != (Real)1) x = mk(x.x * scale, x.y * scale);
-        out[out_base + f + (long long)kk * s_out] = x;
+        if constexpr (MODE == 2) {
+          const int d = kk / a.rows_per_rank;
+          V* dst = reinterpret_cast<V*>(a.peers[d]);
+          dst[out_base + f + (long long)(kk - d * a.rows_per_rank) * s_out] = x;
+        } else {
+          out[out_base + f + (long long)kk * s_out] = x;
+        }
       }
     }
   }

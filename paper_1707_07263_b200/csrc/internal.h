@@ -44,6 +44,16 @@ struct Pass {
   long long lw_n, lw_total;  // K_BITREV/K_LEVEL: transform length, elements (or half) in the batch
 };
 
+// Distributed four-step, pass 1 on one rank (see tilefft_dist_* in the C ABI).
+struct DistPass1 {
+  int L;                    // N1 (column FFT length)
+  long long C;              // columns per rank (N2 / G)
+  size_t tw_off, wc_off, wf_off;
+  int fb;
+  uint32_t m_mask;          // N - 1
+  tfb::CombTmaArgs a;       // mode-2 arguments (peers, pitch, col_off, r_off, ...)
+};
+
 // Kernel launchers, explicitly instantiated in kern_*.cu (one TU per
 // precision/direction so the heavy template instantiation builds in parallel).
 template <typename Real, bool INV>
@@ -62,10 +72,22 @@ template <typename Real>
 int launch_interstage(const void* in, void* out, long long rows, long long cols, long long row0, long long rps,
                       long long sub_len, const void* tbl, long long tstride, cudaStream_t st);
 
+template <typename Real, bool INV>
+int launch_dist_pass1(const DistPass1& d, const void* in, const void* tb, const void* tb64, Real scale,
+                      cudaStream_t st);
+
 extern template int launch_fast<float, false>(const Pass&, const void*, void*, const void*, const void*, float, cudaStream_t);
 extern template int launch_fast<float, true>(const Pass&, const void*, void*, const void*, const void*, float, cudaStream_t);
 extern template int launch_fast<double, false>(const Pass&, const void*, void*, const void*, const void*, double, cudaStream_t);
 extern template int launch_fast<double, true>(const Pass&, const void*, void*, const void*, const void*, double, cudaStream_t);
+extern template int launch_dist_pass1<float, false>(const DistPass1&, const void*, const void*, const void*, float,
+                                                   cudaStream_t);
+extern template int launch_dist_pass1<float, true>(const DistPass1&, const void*, const void*, const void*, float,
+                                                  cudaStream_t);
+extern template int launch_dist_pass1<double, false>(const DistPass1&, const void*, const void*, const void*, double,
+                                                    cudaStream_t);
+extern template int launch_dist_pass1<double, true>(const DistPass1&, const void*, const void*, const void*, double,
+                                                   cudaStream_t);
 extern template int launch_exact<float>(const Pass&, const void*, void*, const void*, float, int, int, cudaStream_t);
 extern template int launch_levelwise<float>(const Pass&, const void*, void*, const void*, float, int, int,
                                            cudaStream_t);

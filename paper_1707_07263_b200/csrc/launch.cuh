@@ -225,6 +225,53 @@ int launch_fast(const Pass& ps, const void* in, void* out, const void* tb, const
   return fail(TILEFFT_EINVAL, "internal: no kernel for pass length %d", ps.L);
 }
 
+// Distributed pass 1: column FFTs of the rank's slab [N1][C], inter-pass root
+// W_N^{r k}, results scattered into the destination slabs (peer memory over
+// NVLink, or local staging for the NCCL exchange).
+template <typename Real, int L, bool INV>
+int launch_dist_pass1_L(const DistPass1& d, const void* in, const void* tb, const void* tb64, Real scale,
+                        cudaStream_t st) {
+  using V = tfb::C2<Real>;
+  using Cfg = tfb::CombTmaCfg<Real, L>;
+  constexpr int W = (int)sizeof(V) / 8;
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((uintptr_t)in % 16) return fail(TILEFFT_EINVAL, "distributed pass 1: input must be 16-byte aligned");
+  CUtensorMap map;
+  const long long vb = (long long)sizeof(V);
+  const cuuint64_t dims[4] = {(cuuint64_t)(d.C * W), (cuuint64_t)L, 1, 1};
+  const cuuint64_t strides[3] = {(cuuint64_t)(d.C * vb), (cuuint64_t)(L * d.C * vb), (cuuint64_t)(L * d.C * vb)};
+  const cuuint32_t box[4] = {(cuuint32_t)(Cfg::F * W), (cuuint32_t)Cfg::BL, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(in), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled failed for the distributed slab");
+  auto k = tfb::k_comb_tma<Real, L, INV, true, 2>;
+  if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
+  int bps = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, Cfg::THREADS, Cfg::SMEM));
+  const long long grid = std::max<long long>(1, std::min<long long>(d.a.ntiles, (long long)sm_count() * std::max(bps, 1)));
+  const V* t = (const V*)tb;
+  const double2* t64 = (const double2*)tb64;
+  k<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, st>>>(map, nullptr, d.a, t + d.tw_off, t64 + d.wc_off, t64 + d.wf_off,
+                                                     scale);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <typename Real, bool INV>
+int launch_dist_pass1(const DistPass1& d, const void* in, const void* tb, const void* tb64, Real scale,
+                      cudaStream_t st) {
+  switch (d.L) {
+    case 128: return launch_dist_pass1_L<Real, 128, INV>(d, in, tb, tb64, scale, st);
+    case 256: return launch_dist_pass1_L<Real, 256, INV>(d, in, tb, tb64, scale, st);
+    case 512: return launch_dist_pass1_L<Real, 512, INV>(d, in, tb, tb64, scale, st);
+    case 1024: return launch_dist_pass1_L<Real, 1024, INV>(d, in, tb, tb64, scale, st);
+  }
+  return fail(TILEFFT_EINVAL, "distributed pass 1: unsupported column length %d", d.L);
+}
+
 template <typename Real>
 int launch_exact(const Pass& ps, const void* in, void* out, const void* tb, Real scale, int conj_in, int conj_out,
                  cudaStream_t st) {

@@ -136,7 +136,15 @@ struct tilefft_plan_s {
   cudaEvent_t hev[3] = {nullptr, nullptr, nullptr};
   DevBuf hbuf[3];
   uint64_t host_chunk = 0;  // transforms per pipelined chunk
+  // distributed four-step (tilefft_dist_*)
+  bool is_dist = false;
+  uint32_t nranks = 1, rank = 0;
+  uint64_t n1 = 0, n2 = 0;
+  DistPass1 dist{};
+  bool peers_set = false;
+  tilefft_plan_s* inner = nullptr;  // row FFTs of length n2 over the rank's n1/nranks rows
   ~tilefft_plan_s() {
+    if (inner) tilefft_plan_destroy(inner);
     for (int i = 0; i < 3; ++i) {
       if (hs[i]) cudaStreamDestroy(hs[i]);
       if (hev[i]) cudaEventDestroy(hev[i]);
@@ -769,6 +777,148 @@ int tilefft_interstage_scale(const void* h_in, void* h_out, uint64_t rows, uint6
     CUDA_TRY(cudaDeviceSynchronize());
     return 0;
   });
+}
+
+// ---------------------------------------------------------------- distributed
+int tilefft_dist_plan_create(tilefft_plan_t* out, uint64_t n, uint32_t nranks, uint32_t rank, uint32_t elem_bytes,
+                             int device) {
+  g_err.clear();
+  if (!out) return fail(TILEFFT_EINVAL, "tilefft_dist_plan_create: null plan pointer");
+  *out = nullptr;
+  if (!is_pow2(n) || n < 2) return fail(TILEFFT_EINVAL, "make_plan: n must be a power of two >= 2");
+  if (!is_pow2(nranks) || nranks > 16 || rank >= nranks)
+    return fail(TILEFFT_EINVAL, "tilefft_dist_plan_create: nranks must be a power of two <= 16 and rank < nranks");
+  if (elem_bytes != 8 && elem_bytes != 16) return fail(TILEFFT_EINVAL, "tilefft_dist_plan_create: elem_bytes must be 8 or 16");
+  const uint64_t F = elem_bytes == 8 ? 16 : 8;
+  // four-step split N = N1 x N2: N1 <= 1024 column FFTs (one on-chip pass),
+  // N2 = N / N1 row FFTs (local multi-pass when > 8192)
+  const uint64_t n1 = std::min<uint64_t>(1024, n >> 7);
+  const uint64_t n2 = n / std::max<uint64_t>(n1, 1);
+  if (n1 < 128 || n1 % nranks || n2 % (nranks * F))
+    return fail(TILEFFT_EINVAL, "tilefft_dist_plan_create: n too small for %u ranks (need n >= %llu)", nranks,
+                (unsigned long long)(128 * 128 * nranks));
+  if (n > (1ull << 32)) return fail(TILEFFT_EINVAL, "tilefft_dist_plan_create: n > 2^32 not supported");
+  if (int rc = check_device(device)) return rc;
+  tilefft_plan_s* P = new (std::nothrow) tilefft_plan_s();
+  if (!P) return fail(TILEFFT_ENOMEM, "out of host memory");
+  P->device = device;
+  P->is_dist = true;
+  P->n = n;
+  P->batch = 1;
+  P->elem_bytes = elem_bytes;
+  P->nranks = nranks;
+  P->rank = rank;
+  P->n1 = n1;
+  P->n2 = n2;
+  TableBuilder<double> tb64;
+  P->tb64 = &tb64;
+  auto build = [&](auto tbv) -> int {
+    using Real = std::remove_reference_t<decltype(tbv.h[0])>;
+    TableBuilder<Real> tb;
+    DistPass1& d = P->dist;
+    d.L = (int)n1;
+    d.C = (long long)(n2 / nranks);
+    d.tw_off = add_stage_table(tb, (int)n1);
+    add_interpass(tb64, n, &d.wc_off, &d.wf_off, &d.fb);
+    d.m_mask = (uint32_t)(n - 1);
+    tfb::CombTmaArgs& a = d.a;
+    a.chunks = d.C / (long long)F;
+    a.groups_per_batch = 1;
+    a.ntiles = a.chunks;
+    a.rps = d.C;
+    a.sub_len = (long long)(n1 * d.C);
+    a.fvalid = (int)F;
+    a.fb = d.fb;
+    a.m_mask = d.m_mask;
+    a.r_off = (long long)rank * d.C;
+    a.rows_per_rank = (int)(n1 / nranks);
+    a.nranks = (int)nranks;
+    P->dev_factors = {n1};
+    int rc = finish_plan<Real>(P, tb);
+    if (rc) return rc;
+    return tilefft_plan_create(&P->inner, n2, n1 / nranks, nullptr, 0, elem_bytes, TILEFFT_MODE_FAST, nullptr, 0,
+                               device);
+  };
+  int rc = elem_bytes == 8 ? build(TableBuilder<float>{}) : build(TableBuilder<double>{});
+  P->tb64 = nullptr;
+  if (rc) {
+    delete P;
+    return rc;
+  }
+  for (uint64_t f : P->inner->dev_factors) P->dev_factors.push_back(f);
+  *out = P;
+  return 0;
+}
+
+int tilefft_dist_layout(tilefft_plan_t P, uint64_t* n1, uint64_t* n2, uint64_t* cols_per_rank, uint64_t* rows_per_rank) {
+  if (!P || !P->is_dist) return fail(TILEFFT_EINVAL, "tilefft_dist_layout: not a distributed plan");
+  if (n1) *n1 = P->n1;
+  if (n2) *n2 = P->n2;
+  if (cols_per_rank) *cols_per_rank = P->n2 / P->nranks;
+  if (rows_per_rank) *rows_per_rank = P->n1 / P->nranks;
+  return 0;
+}
+
+int tilefft_dist_set_peers(tilefft_plan_t P, void* const* dest, uint32_t ndest, uint64_t row_pitch, uint64_t col_off) {
+  g_err.clear();
+  if (!P || !P->is_dist) return fail(TILEFFT_EINVAL, "tilefft_dist_set_peers: not a distributed plan");
+  if (!dest || ndest != P->nranks) return fail(TILEFFT_EINVAL, "tilefft_dist_set_peers: need one destination per rank");
+  for (uint32_t i = 0; i < ndest; ++i) {
+    if (!dest[i]) return fail(TILEFFT_EINVAL, "tilefft_dist_set_peers: null destination");
+    P->dist.a.peers[i] = dest[i];
+  }
+  P->dist.a.pitch = (long long)row_pitch;
+  P->dist.a.col_off = (long long)col_off;
+  P->peers_set = true;
+  return 0;
+}
+
+int tilefft_dist_exec_pass1(tilefft_plan_t P, const void* d_slab, int sign, void* stream) {
+  g_err.clear();
+  if (!P || !P->is_dist) return fail(TILEFFT_EINVAL, "tilefft_dist_exec_pass1: not a distributed plan");
+  if (!P->peers_set) return fail(TILEFFT_EINVAL, "tilefft_dist_exec_pass1: destinations not set");
+  if (!d_slab) return fail(TILEFFT_EINVAL, "tilefft_dist_exec_pass1: null input");
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool inv = sign == TILEFFT_INVERSE;
+  if (P->elem_bytes == 8) {
+    const float s = inv ? 1.0f / (float)P->n1 : 1.0f;
+    return inv ? launch_dist_pass1<float, true>(P->dist, d_slab, P->tables.p, P->tables64.p, s, st)
+               : launch_dist_pass1<float, false>(P->dist, d_slab, P->tables.p, P->tables64.p, s, st);
+  }
+  const double s = inv ? 1.0 / (double)P->n1 : 1.0;
+  return inv ? launch_dist_pass1<double, true>(P->dist, d_slab, P->tables.p, P->tables64.p, s, st)
+             : launch_dist_pass1<double, false>(P->dist, d_slab, P->tables.p, P->tables64.p, s, st);
+}
+
+int tilefft_dist_exec_pass2(tilefft_plan_t P, const void* d_rows, void* d_out, int sign, void* stream) {
+  g_err.clear();
+  if (!P || !P->is_dist) return fail(TILEFFT_EINVAL, "tilefft_dist_exec_pass2: not a distributed plan");
+  return tilefft_exec_c2c(P->inner, d_rows, d_out, sign, stream);
+}
+
+int tilefft_ipc_get_handle(const void* dptr, void* handle_out) {
+  g_err.clear();
+  if (!dptr || !handle_out) return fail(TILEFFT_EINVAL, "tilefft_ipc_get_handle: null argument");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+  std::memcpy(handle_out, &h, sizeof h);
+  return 0;
+}
+
+int tilefft_ipc_open_handle(const void* handle, void** dptr) {
+  g_err.clear();
+  if (!handle || !dptr) return fail(TILEFFT_EINVAL, "tilefft_ipc_open_handle: null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  CUDA_TRY(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+
+int tilefft_ipc_close_handle(void* dptr) {
+  g_err.clear();
+  CUDA_TRY(cudaIpcCloseMemHandle(dptr));
+  return 0;
 }
 
 int tilefft_plan_destroy(tilefft_plan_t P) {

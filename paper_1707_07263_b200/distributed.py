@@ -1,0 +1,162 @@
+"""Multi-GPU execution.
+
+* Batched / 2D transforms shard the batch (or the images) over ranks with no
+  collective on the data path: ``shard_rows`` gives each rank its contiguous
+  share and results are bit-identical to the single-GPU run (the GPU kernels do
+  not depend on how many transforms a launch holds — the same thread-count
+  invariance the reference guarantees, test_tiled_fft.cpp:236-253).
+
+* A single 1D transform too large for one GPU runs as a four-step transform
+  N = N1 x N2 over G ranks (``DistributedFFT``): the reference's own pass
+  structure lifted to GPUs. Pass 1 (the comb pass, tiled_fft.hpp:252-294:
+  column FFTs of length N1 plus the inter-pass root W_N^{r k1}) runs on the
+  rank's column slab, and its store IS the exchange — spectrum row k1 belongs
+  to rank k1 / (N1/G) (stage_plan.hpp:164-170). Two exchange transports:
+    - ``"p2p"``: the pass-1 kernel writes its results straight into the other
+      ranks' row slabs, mapped into this process with CUDA IPC, so the
+      transpose rides NVLink inside the kernel, overlapped tile by tile with the
+      butterflies (the fused compute + all-to-all);
+    - ``"nccl"``: pass 1 writes per-destination staging blocks, then one
+      ``all_to_all_single`` (NCCL grouped send/recv) and a local re-assembly.
+  Pass 2 is the row FFT of length N2 on the rank's row slab (local multi-pass).
+
+Layouts (rank g, C = N2/G, R = N1/G):
+  input  column slab [N1][C]:  x[g*C + c + N2*n1]
+  output row slab    [R][N2]:  X[(g*R + k1) + N1*k2]   (digit-interleaved slabs)
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _capi
+
+
+def shard_rows(total: int, world: int, rank: int):
+    """Contiguous [begin, end) share of `total` independent transforms."""
+    base, extra = divmod(total, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+def four_step_layout(n: int, world: int):
+    """(N1, N2, C, R) of the distributed split (mirrors tilefft_dist_plan_create)."""
+    n1 = min(1024, n >> 7)
+    n2 = n // n1
+    return n1, n2, n2 // world, n1 // world
+
+
+def column_slab(x: np.ndarray, world: int, rank: int) -> np.ndarray:
+    """Rank `rank`'s input slab [N1][C] of a natural-order signal x."""
+    n1, n2, c, _ = four_step_layout(x.shape[-1], world)
+    return np.ascontiguousarray(x.reshape(n1, n2)[:, rank * c:(rank + 1) * c])
+
+
+def assemble_output(slabs, n: int) -> np.ndarray:
+    """Natural-order spectrum from every rank's row slab [R][N2]."""
+    world = len(slabs)
+    n1, n2, _, r = four_step_layout(n, world)
+    rows = np.concatenate([np.asarray(s).reshape(r, n2) for s in slabs], axis=0)  # [k1][k2]
+    return np.ascontiguousarray(rows.T).reshape(n)  # X[k1 + N1*k2]
+
+
+class GpuOps:
+    """The rank-local steps on the B200 through the C ABI."""
+
+    def __init__(self, n, world, rank, device, elem_bytes=8):
+        import torch
+        self.torch = torch
+        self.device = device
+        self.plan = _capi.DistPlan.create_dist(n, world, rank, elem_bytes, device)
+        lay = self.plan.layout()
+        self.n1, self.n2, self.c, self.r = lay["n1"], lay["n2"], lay["cols_per_rank"], lay["rows_per_rank"]
+        self.dtype = torch.complex64 if elem_bytes == 8 else torch.complex128
+
+    def alloc(self, shape):
+        return self.torch.empty(shape, dtype=self.dtype, device=f"cuda:{self.device}")
+
+    @staticmethod
+    def ptr(t):
+        return t.data_ptr()
+
+    def set_dests(self, ptrs, pitch, col_off):
+        self.plan.set_peers(ptrs, pitch, col_off)
+
+    def stream(self):
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def pass1(self, slab, sign):
+        self.plan.pass1(slab.data_ptr(), sign, self.stream())
+
+    def pass2(self, rows, out, sign):
+        self.plan.pass2(rows.data_ptr(), out.data_ptr(), sign, self.stream())
+
+    def sync(self):
+        self.torch.cuda.synchronize(self.device)
+
+    def ipc_handle(self, t):
+        return _capi.ipc_handle(t.data_ptr())
+
+    def ipc_open(self, h):
+        return _capi.ipc_open(h)
+
+
+class DistributedFFT:
+    """One length-n transform over the ranks of ``torch.distributed`` (or a
+    single process when it is not initialised)."""
+
+    def __init__(self, n: int, exchange: str = "p2p", ops=None, device: int = 0, elem_bytes: int = 8):
+        import torch.distributed as dist
+        self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        self.world = self.dist.get_world_size() if self.dist else 1
+        self.rank = self.dist.get_rank() if self.dist else 0
+        self.n = n
+        self.exchange = exchange if self.world > 1 else "local"
+        self.ops = ops or GpuOps(n, self.world, self.rank, device, elem_bytes)
+        o = self.ops
+        self.rows = o.alloc((o.r, o.n2))
+        self._opened = []
+        if self.exchange == "local":
+            o.set_dests([o.ptr(self.rows)], o.n2, 0)
+        elif self.exchange == "p2p":
+            handles = [None] * self.world
+            self.dist.all_gather_object(handles, o.ipc_handle(self.rows))
+            ptrs = []
+            for g, h in enumerate(handles):
+                if g == self.rank:
+                    ptrs.append(o.ptr(self.rows))
+                else:
+                    p = o.ipc_open(h)
+                    self._opened.append(p)
+                    ptrs.append(p)
+            o.set_dests(ptrs, o.n2, self.rank * o.c)
+        elif self.exchange == "nccl":
+            self.stage = o.alloc((self.world, o.r, o.c))
+            self.recv = o.alloc((self.world, o.r, o.c))
+            o.set_dests([o.ptr(self.stage[d]) for d in range(self.world)], o.c, 0)
+        else:
+            raise ValueError(f"unknown exchange {exchange!r}")
+
+    def forward(self, col_slab, out=None, inverse: bool = False):
+        """col_slab: this rank's [N1][C] slab; returns its [R][N2] output slab."""
+        o = self.ops
+        sign = _capi.INVERSE if inverse else _capi.FORWARD
+        if out is None:
+            out = o.alloc((o.r, o.n2))
+        o.pass1(col_slab, sign)
+        if self.exchange == "p2p":
+            o.sync()              # this rank's peer stores are complete ...
+            self.dist.barrier()   # ... and so are everyone else's into our slab
+        elif self.exchange == "nccl":
+            self.dist.all_to_all_single(self.recv, self.stage)
+            for s in range(self.world):  # [src][k1][c] -> [k1][src*C + c]
+                self.rows[:, s * o.c:(s + 1) * o.c] = self.recv[s]
+        o.pass2(self.rows, out, sign)
+        return out
+
+    def close(self):
+        for p in self._opened:
+            try:
+                _capi.ipc_close(p)
+            except Exception:
+                pass
+        self._opened = []
