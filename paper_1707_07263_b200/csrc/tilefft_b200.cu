@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -132,9 +133,12 @@ struct tilefft_plan_s {
   size_t table_elems = 0;
   // host-path staging
   std::mutex host_mu;
-  cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
-  cudaEvent_t hev[3] = {nullptr, nullptr, nullptr};
-  DevBuf hbuf[3];
+  static constexpr int kHostStreams = 4;
+  cudaStream_t hs[kHostStreams] = {};
+  cudaEvent_t hev[kHostStreams] = {};     // D2H of buffer i done
+  cudaEvent_t hev_in[kHostStreams] = {};  // H2D of buffer i done
+  cudaEvent_t hev_k[kHostStreams] = {};   // kernel on buffer i done
+  DevBuf hbuf[kHostStreams];
   uint64_t host_chunk = 0;  // transforms per pipelined chunk
   // distributed four-step (tilefft_dist_*)
   bool is_dist = false;
@@ -145,9 +149,11 @@ struct tilefft_plan_s {
   tilefft_plan_s* inner = nullptr;  // row FFTs of length n2 over the rank's n1/nranks rows
   ~tilefft_plan_s() {
     if (inner) tilefft_plan_destroy(inner);
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < kHostStreams; ++i) {
       if (hs[i]) cudaStreamDestroy(hs[i]);
       if (hev[i]) cudaEventDestroy(hev[i]);
+      if (hev_in[i]) cudaEventDestroy(hev_in[i]);
+      if (hev_k[i]) cudaEventDestroy(hev_k[i]);
     }
   }
 };
@@ -688,39 +694,77 @@ int tilefft_exec_c2c_host(tilefft_plan_t P, const void* h_in, void* h_out, int s
     CUDA_TRY(cudaMemcpy(h_out, P->hbuf[0].p, bytes, cudaMemcpyDeviceToHost));
     return 0;
   }
-  // ~32 MiB chunks over 3 streams: H2D(i+1) || kernel(i) || D2H(i-1)
+  // Three-queue pipeline over kHostStreams device buffers of ~16 MiB:
+  //   hs[0]: H2D copies, back to back (one copy engine)
+  //   hs[1]: the pass kernel, in place on the chunk
+  //   hs[2]: D2H copies, back to back (the other copy engine)
+  // events order the queues per buffer, so both PCIe directions stream at once
+  // and only the first H2D and the last D2H chunk are not overlapped.
+  constexpr int NB = tilefft_plan_s::kHostStreams;
   if (!P->host_chunk) {
-    uint64_t c = std::max<uint64_t>(1, (32ull << 20) / (per * eb));
+    uint64_t chunk_mb = 32;
+    if (const char* e = std::getenv("TILEFFT_HOST_CHUNK_MB")) chunk_mb = std::max(1, std::atoi(e));
+    uint64_t c = std::max<uint64_t>(1, (chunk_mb << 20) / (per * eb));
     P->host_chunk = std::min<uint64_t>(c, B);
-    for (int i = 0; i < 3; ++i) {
-      CUDA_TRY(cudaStreamCreateWithFlags(&P->hs[i], cudaStreamNonBlocking));
+    for (int i = 0; i < 3; ++i) CUDA_TRY(cudaStreamCreateWithFlags(&P->hs[i], cudaStreamNonBlocking));
+    for (int i = 0; i < NB; ++i) {
       if (int rc = P->hbuf[i].alloc(P->host_chunk * per * eb)) return rc;
+      CUDA_TRY(cudaEventCreateWithFlags(&P->hev[i], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&P->hev_in[i], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&P->hev_k[i], cudaEventDisableTiming));
     }
   }
-  const uint64_t C = P->host_chunk;
+  // chunk schedule: ramp up from C/8 and back down at the end, so the
+  // non-overlapped first H2D and last D2H are short while the steady state
+  // uses large copies (each copy has ~18 us of fixed cost)
+  const uint64_t Cmax = P->host_chunk;
+  std::vector<uint64_t> sizes;
+  {
+    std::vector<uint64_t> head, tail;
+    uint64_t left = B;
+    for (uint64_t c = std::max<uint64_t>(1, Cmax / 8); c < Cmax && left > 2 * c; c *= 2) {
+      head.push_back(c);
+      tail.push_back(c);
+      left -= 2 * c;
+    }
+    sizes = head;
+    while (left > 0) {
+      const uint64_t c = std::min(left, Cmax);
+      sizes.push_back(c);
+      left -= c;
+    }
+    for (auto it = tail.rbegin(); it != tail.rend(); ++it) sizes.push_back(*it);
+  }
   Pass ps = P->passes[0];
-  int ci = 0;
-  for (uint64_t b0 = 0; b0 < B; b0 += C, ci = (ci + 1) % 3) {
-    const uint64_t nb = std::min<uint64_t>(C, B - b0);
+  uint64_t b0 = 0;
+  for (uint64_t idx = 0; idx < sizes.size(); b0 += sizes[idx], ++idx) {
+    const int bi = (int)(idx % NB);
+    const uint64_t nb = sizes[idx];
     const size_t off = b0 * per * eb, bytes = nb * per * eb;
-    cudaStream_t st = P->hs[ci];
-    CUDA_TRY(cudaMemcpyAsync(P->hbuf[ci].p, (const char*)h_in + off, bytes, cudaMemcpyHostToDevice, st));
+    void* buf = P->hbuf[bi].p;
+    if (idx >= (uint64_t)NB) CUDA_TRY(cudaStreamWaitEvent(P->hs[0], P->hev[bi], 0));  // buffer drained
+    CUDA_TRY(cudaMemcpyAsync(buf, (const char*)h_in + off, bytes, cudaMemcpyHostToDevice, P->hs[0]));
+    CUDA_TRY(cudaEventRecord(P->hev_in[bi], P->hs[0]));
+    CUDA_TRY(cudaStreamWaitEvent(P->hs[1], P->hev_in[bi], 0));
     ps.nrows = (long long)nb;
     const bool inv = sign == TILEFFT_INVERSE;
     int rc;
     if (P->elem_bytes == 8) {
       const float scale = inv ? 1.0f / (float)per : 1.0f;
-      rc = inv ? launch_fast<float, true>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, nullptr, scale, st)
-               : launch_fast<float, false>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, nullptr, scale, st);
+      rc = inv ? launch_fast<float, true>(ps, buf, buf, P->tables.p, nullptr, scale, P->hs[1])
+               : launch_fast<float, false>(ps, buf, buf, P->tables.p, nullptr, scale, P->hs[1]);
     } else {
       const double scale = inv ? 1.0 / (double)per : 1.0;
-      rc = inv ? launch_fast<double, true>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, nullptr, scale, st)
-               : launch_fast<double, false>(ps, P->hbuf[ci].p, P->hbuf[ci].p, P->tables.p, nullptr, scale, st);
+      rc = inv ? launch_fast<double, true>(ps, buf, buf, P->tables.p, nullptr, scale, P->hs[1])
+               : launch_fast<double, false>(ps, buf, buf, P->tables.p, nullptr, scale, P->hs[1]);
     }
     if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync((char*)h_out + off, P->hbuf[ci].p, bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(P->hev_k[bi], P->hs[1]));
+    CUDA_TRY(cudaStreamWaitEvent(P->hs[2], P->hev_k[bi], 0));
+    CUDA_TRY(cudaMemcpyAsync((char*)h_out + off, buf, bytes, cudaMemcpyDeviceToHost, P->hs[2]));
+    CUDA_TRY(cudaEventRecord(P->hev[bi], P->hs[2]));
   }
-  for (int i = 0; i < 3; ++i) CUDA_TRY(cudaStreamSynchronize(P->hs[i]));
+  CUDA_TRY(cudaStreamSynchronize(P->hs[2]));
   return 0;
 }
 
