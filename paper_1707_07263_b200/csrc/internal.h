@@ -7,6 +7,8 @@
 
 #include "exact_kernels.cuh"
 #include "fast_kernels.cuh"
+#include "twolevel.cuh"
+#include "comb_w.cuh"
 #include "../../include/tilefft_b200.h"
 
 namespace tfb_host {
@@ -23,7 +25,7 @@ int fail(int code, const char* fmt, ...);
 // Opt a kernel into >48 KB dynamic shared memory (once per function/device).
 int ensure_smem(const void* fn, int bytes);
 
-enum PassKind { K_ROWS = 0, K_COMB1D = 1, K_COMBAX = 2, K_FINALT = 3, K_EXACT = 4, K_BITREV = 5, K_LEVEL = 6 };
+enum PassKind { K_ROWS = 0, K_COMB1D = 1, K_COMBAX = 2, K_FINALT = 3, K_EXACT = 4, K_BITREV = 5, K_LEVEL = 6, K_TWO = 7 };
 
 struct Pass {
   PassKind kind;
@@ -42,6 +44,12 @@ struct Pass {
   bool no_tma;               // force the register-only K_ROWS variant
   int level;                 // K_LEVEL: radix-2 level (h = 2^level)
   long long lw_n, lw_total;  // K_BITREV/K_LEVEL: transform length, elements (or half) in the batch
+  // K_TWO (two-level pass through L2, twolevel.cuh)
+  tfb::TwoArgs two;
+  int la, lb, outt;
+  long long two_cols, two_es_in;  // columns along the axis and their element stride (input)
+  size_t twl_off;                 // W_L^e table (L entries)
+  int two_ctas;                   // persistent grid
 };
 
 // Distributed four-step, pass 1 on one rank (see tilefft_dist_* in the C ABI).

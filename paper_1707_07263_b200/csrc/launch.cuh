@@ -1,6 +1,8 @@
 // Kernel launchers (templates); instantiated per precision/direction in kern_*.cu.
 #pragma once
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 #include <cudaTypedefs.h>
 
@@ -75,6 +77,14 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+// The warp-owned comb kernel (comb_w.cuh) is opt-in: measured slower than
+// K_COMB_TMA at 2^26 (0.78 vs 0.66 ms; 8 consumer warps per SM leave the
+// twiddle and exchange latencies exposed).
+inline bool comb_w_disabled() {
+  const char* e = std::getenv("TILEFFT_COMBW");
+  return !(e && *e && *e != '0');
+}
+
 inline int sm_count() {
   static int n[16] = {0};
   int dev = 0;
@@ -122,9 +132,88 @@ bool encode_comb_map(CUtensorMap* map, const Pass& ps, const void* in) {
   return r == CUDA_SUCCESS;
 }
 
+// Warp-owned comb pass (comb_w.cuh): fp32, 64 <= L <= 512, F = 8192 / L
+// adjacent combs per tile. Returns 1 when the geometry does not fit (the
+// caller then uses K_COMB_TMA / K_COMB).
+template <int L, bool INV>
+int launch_comb_w(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, float scale,
+                  cudaStream_t st) {
+  using Cfg = tfb::CombWCfg<L>;
+  constexpr int F = Cfg::F;
+  auto enc = tensor_map_encoder();
+  const tfb::CombArgs& c = ps.comb;
+  const bool ax = ps.kind == K_COMBAX;
+  const long long ncols = ax ? c.es : c.rps;
+  if (!enc || ((uintptr_t)in % 16) || ((uintptr_t)out % 16) || ncols % F) return 1;
+  const long long B = c.ntiles / (c.chunks * c.groups_per_batch);
+  tfb::CombTmaArgs a{};
+  a.chunks = ncols / F;
+  a.groups_per_batch = c.groups_per_batch;
+  a.ntiles = a.chunks * c.groups_per_batch * B;
+  a.rps = c.rps;
+  a.sub_len = c.sub_len;
+  a.es = c.es;
+  a.bstride = c.bstride;
+  a.out_w_last = c.out_w_last;
+  a.final_pass = c.final_pass;
+  a.fvalid = F;
+  a.fb = c.fb;
+  a.p = c.p;
+  a.m_mask = c.m_mask;
+  for (int i = 0; i < 8; ++i) {
+    a.out_w[i] = c.out_w[i];
+    a.sub_w[i] = c.sub_w[i];
+  }
+  cuuint64_t di[4], si[3], dout[4], so[3];
+  if (!ax) {
+    di[0] = (cuuint64_t)c.rps; di[1] = L; di[2] = 1; di[3] = (cuuint64_t)(B * c.groups_per_batch);
+    si[0] = (cuuint64_t)(c.rps * 8); si[1] = (cuuint64_t)(c.sub_len * 8); si[2] = si[1];
+    for (int i = 0; i < 4; ++i) dout[i] = di[i];
+    for (int i = 0; i < 3; ++i) so[i] = si[i];
+  } else {
+    di[0] = (cuuint64_t)c.es; di[1] = L; di[2] = (cuuint64_t)c.rps; di[3] = (cuuint64_t)(B * (c.groups_per_batch / c.rps));
+    si[0] = (cuuint64_t)(c.rps * c.es * 8); si[1] = (cuuint64_t)(c.es * 8); si[2] = (cuuint64_t)(c.sub_len * c.es * 8);
+    if (c.final_pass) {
+      dout[0] = (cuuint64_t)c.es; dout[1] = L; dout[2] = (cuuint64_t)c.out_w_last; dout[3] = (cuuint64_t)B;
+      so[0] = (cuuint64_t)(c.out_w_last * c.es * 8); so[1] = (cuuint64_t)(c.es * 8); so[2] = (cuuint64_t)(c.bstride * 8);
+    } else {
+      for (int i = 0; i < 4; ++i) dout[i] = di[i];
+      for (int i = 0; i < 3; ++i) so[i] = si[i];
+    }
+  }
+  for (int i = 0; i < 3; ++i)
+    if (si[i] % 16 || so[i] % 16 || si[i] >= (1ull << 40) || so[i] >= (1ull << 40)) return 1;
+  const cuuint32_t box[4] = {16, (cuuint32_t)Cfg::BL, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUtensorMap mi, mo;
+  if (enc(&mi, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(in), di, si, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+      enc(&mo, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, out, dout, so, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return 1;
+  auto go = [&](auto k) -> int {
+    if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return -rc;
+    const long long grid = std::max<long long>(1, std::min<long long>(a.ntiles, (long long)sm_count()));
+    k<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, st>>>(mi, mo, a, (const float2*)tb + ps.tw_off,
+                                                      (const double2*)tb64 + ps.wc_off, (const double2*)tb64 + ps.wf_off,
+                                                      scale);
+    if (cudaGetLastError() != cudaSuccess) return -fail(TILEFFT_ECUDA, "k_comb_w launch failed");
+    return 0;
+  };
+  if (!ax) return go(tfb::k_comb_w<L, INV, true, 0>);
+  if (ps.twid) return go(tfb::k_comb_w<L, INV, true, 1>);
+  return go(tfb::k_comb_w<L, INV, false, 1>);
+}
+
 template <typename Real, int L, bool INV>
 int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, Real scale,
                 cudaStream_t st) {
+  if constexpr (std::is_same<Real, float>::value && L >= 64 && L <= 512) {
+    if (!ps.no_tma && !comb_w_disabled()) {
+      const int rc = launch_comb_w<L, INV>(ps, in, out, tb, tb64, scale, st);
+      if (rc <= 0) return -rc;
+    }
+  }
   using V = tfb::C2<Real>;
   const V* t = (const V*)tb;
   const double2* t64 = (const double2*)tb64;
@@ -194,6 +283,73 @@ int launch_final(const Pass& ps, const void* in, void* out, const void* tb, cons
   return 0;
 }
 
+// Two-level pass (fp32): tensor map over the strided axis {column, n1, n2, batch}
+// (128-byte swizzle for the transposed-output variant), control block reset,
+// persistent launch.
+template <int LA, int LB, bool INV, int OUTT, bool TWID>
+int launch_two_k(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, float scale,
+                 cudaStream_t st) {
+  using Cfg = tfb::TwoCfg<LA, LB, INV, OUTT>;
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((uintptr_t)in % 16) return fail(TILEFFT_EINVAL, "two-level pass: input must be 16-byte aligned");
+  const tfb::TwoArgs& a = ps.two;
+  const long long B = a.groups / a.chunks;
+  CUtensorMap map;
+  const cuuint64_t dims[4] = {(cuuint64_t)ps.two_cols, (cuuint64_t)LB, (cuuint64_t)LA, (cuuint64_t)B};
+  const cuuint64_t strides[3] = {(cuuint64_t)(ps.two_es_in * 8), (cuuint64_t)(ps.two_es_in * 8 * LB),
+                                 (cuuint64_t)(a.bs_in * 8)};
+  const cuuint32_t box[4] = {16, 1, (cuuint32_t)Cfg::BL, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(in), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, OUTT ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled failed for the two-level pass");
+  auto k = tfb::k_two<LA, LB, INV, OUTT, TWID>;
+  if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
+  static int occ[16] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!occ[dev & 15]) {
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev & 15], k, 256, Cfg::SMEM));
+    if (occ[dev & 15] < 1) return fail(TILEFFT_ECUDA, "two-level pass: kernel does not fit on an SM");
+  }
+  const int grid = sm_count() * occ[dev & 15];
+  CUDA_TRY(cudaMemsetAsync(a.ctrl, 0, sizeof(unsigned) * (1 + 2 * a.nslot), st));
+  const float2* t = (const float2*)tb;
+  const double2* t64 = (const double2*)tb64;
+  k<<<grid, 256, Cfg::SMEM, st>>>(map, (float2*)out, a, t + ps.tw_off, t + ps.twl_off, t64 + ps.wc_off,
+                                  t64 + ps.wf_off, scale);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <int LA, int LB, bool INV>
+int launch_two_l(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, float scale,
+                 cudaStream_t st) {
+  if (ps.outt) {
+    return ps.twid ? launch_two_k<LA, LB, INV, 1, true>(ps, in, out, tb, tb64, scale, st)
+                   : launch_two_k<LA, LB, INV, 1, false>(ps, in, out, tb, tb64, scale, st);
+  }
+  return ps.twid ? launch_two_k<LA, LB, INV, 0, true>(ps, in, out, tb, tb64, scale, st)
+                 : launch_two_k<LA, LB, INV, 0, false>(ps, in, out, tb, tb64, scale, st);
+}
+
+template <typename Real, bool INV>
+int launch_two(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, Real scale,
+               cudaStream_t st) {
+  if constexpr (std::is_same<Real, float>::value) {
+    if (ps.la == 512) {
+      switch (ps.lb) {
+        case 4: return launch_two_l<512, 4, INV>(ps, in, out, tb, tb64, scale, st);
+        case 8: return launch_two_l<512, 8, INV>(ps, in, out, tb, tb64, scale, st);
+        case 16: return launch_two_l<512, 16, INV>(ps, in, out, tb, tb64, scale, st);
+      }
+    }
+  }
+  return fail(TILEFFT_EINVAL, "internal: no two-level kernel for %d x %d", ps.la, ps.lb);
+}
+
 template <typename Real, bool INV>
 int launch_fast(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, Real scale,
                 cudaStream_t st) {
@@ -220,6 +376,8 @@ int launch_fast(const Pass& ps, const void* in, void* out, const void* tb, const
     DISPATCH(launch_comb)
   } else if (ps.kind == K_FINALT) {
     DISPATCH(launch_final)
+  } else if (ps.kind == K_TWO) {
+    return launch_two<Real, INV>(ps, in, out, tb, tb64, scale, st);
   }
 #undef DISPATCH
   return fail(TILEFFT_EINVAL, "internal: no kernel for pass length %d", ps.L);

@@ -130,6 +130,8 @@ struct tilefft_plan_s {
   DevBuf tables64;        // fp64 inter-pass root tables
   TableBuilder<double>* tb64 = nullptr;  // plan-build scratch
   DevBuf work;            // workspace (batch * n elements)
+  std::vector<Pass> passes_alt;  // same transform without two-level passes (used when the input is not 16-B aligned)
+  DevBuf scratch, ctrl;   // two-level passes: L2-resident exchange slots and their counters
   size_t table_elems = 0;
   // host-path staging
   std::mutex host_mu;
@@ -241,6 +243,89 @@ std::vector<uint64_t> balanced_factors(uint64_t n, uint64_t cap) {
   return f;
 }
 
+
+// ---------------------------------------------------------------- two-level passes
+bool env_flag(const char* name) {
+  const char* e = std::getenv(name);
+  return e && *e && *e != '0';
+}
+// Two-level passes: on by default for 2D columns (8192^2: 2 HBM passes,
+// 0.61 ms vs 0.71 ms for rows + [128, 64] columns); opt-in for 1D, where the
+// 3-pass comb plan is still faster (0.66 ms vs 0.82 ms at 2^26).
+bool two_level_enabled() { return !env_flag("TILEFFT_NO_TWO"); }
+bool two_level_1d_enabled() { return two_level_enabled() && env_flag("TILEFFT_TWO_1D"); }
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? std::atoi(e) : dflt;
+}
+bool two_level_len(uint64_t L) { return L == 2048 || L == 4096 || L == 8192; }
+
+// One K_TWO pass: length-L transforms along an axis with `cols` columns at
+// element stride es_in (16 adjacent columns per group), `B` batch items.
+template <typename Real>
+Pass make_two_pass(tilefft_plan_s* P, TableBuilder<Real>& tb, uint64_t L, long long cols, long long es_in,
+                   long long B, long long bs_in, long long bs_out, long long es_out, int outt, bool twid, uint64_t M) {
+  Pass ps{};
+  ps.kind = K_TWO;
+  ps.L = (int)L;
+  ps.la = 512;
+  ps.lb = (int)(L / 512);
+  ps.outt = outt;
+  ps.twid = twid;
+  ps.tw_off = add_stage_table(tb, 512);
+  ps.twl_off = tb.add(L);
+  for (uint64_t e = 0; e < L; ++e) {
+    Real re, im;
+    acc_root<Real>(e, L, &re, &im);
+    tb.set(ps.twl_off + e, re, im);
+  }
+  tfb::TwoArgs& a = ps.two;
+  if (twid) {
+    add_interpass(*P->tb64, M, &ps.wc_off, &ps.wf_off, &a.fb);
+    a.m_mask = (uint32_t)(M - 1);
+  }
+  a.chunks = cols / 16;
+  a.groups = a.chunks * B;
+  a.bs_in = bs_in;
+  a.bs_out = bs_out;
+  a.es_out = es_out;
+  a.D = std::max(1, env_int("TILEFFT_TWO_D", 24));
+  if (a.D > a.groups) a.D = (int)a.groups;
+  a.nslot = std::max(a.D + 1, env_int("TILEFFT_TWO_NSLOT", 2 * a.D));
+  a.discard = env_int("TILEFFT_TWO_DISCARD", 1);
+  ps.two_cols = cols;
+  ps.two_es_in = es_in;
+  return ps;
+}
+
+// 2^22 <= n <= 2^26 (fp32): the four-step split n = L1 x L2 in two HBM passes,
+// both two-level: pass 1 = L1-point column FFTs (stride L2) times W_n^{c k},
+// stored transposed (row c of a [L2][L1] matrix); pass 2 = L2-point FFTs over
+// those rows' columns, stored in natural order X[k1 + L1 k2].
+template <typename Real>
+bool build_two_1d(tilefft_plan_s* P, TableBuilder<Real>& tb) {
+  if (!std::is_same<Real, float>::value || !two_level_1d_enabled()) return false;
+  const uint64_t n = P->n, B = P->batch;
+  const int b = ilog2(n);
+  const uint64_t L1 = 1ull << ((b + 1) / 2), L2 = n / L1;
+  if (!two_level_len(L1) || !two_level_len(L2)) return false;
+  P->passes_alt = std::move(P->passes);
+  P->passes.clear();
+  Pass p1 = make_two_pass(P, tb, L1, (long long)L2, (long long)L2, (long long)B, (long long)n, (long long)n,
+                          (long long)L1, 1, true, n);
+  p1.src = 0;
+  p1.dst = 2;
+  Pass p2 = make_two_pass(P, tb, L2, (long long)L1, (long long)L1, (long long)B, (long long)n, (long long)n,
+                          (long long)L1, 0, false, 0);
+  p2.src = 2;
+  p2.dst = 1;
+  p2.final_pass = true;
+  P->passes.push_back(p1);
+  P->passes.push_back(p2);
+  P->dev_factors = {L1, L2};
+  return true;
+}
+
 // ---------------------------------------------------------------- plan building
 template <typename Real>
 int build_fast_1d(tilefft_plan_s* P, TableBuilder<Real>& tb) {
@@ -307,6 +392,7 @@ int build_fast_1d(tilefft_plan_s* P, TableBuilder<Real>& tb) {
     P->passes.push_back(ps);
   }
   P->dev_factors = f;
+  build_two_1d<Real>(P, tb);
   return 0;
 }
 
@@ -468,6 +554,23 @@ int finish_plan(tilefft_plan_s* P, TableBuilder<Real>& tb) {
   // workspace when any pass touches it
   bool need_work = false;
   for (const Pass& ps : P->passes) need_work |= (ps.src == 2 || ps.dst == 2);
+  for (const Pass& ps : P->passes_alt) need_work |= (ps.src == 2 || ps.dst == 2);
+  size_t scratch_elems = 0;
+  int ctrl_words = 0;
+  for (const Pass& ps : P->passes)
+    if (ps.kind == K_TWO) {
+      scratch_elems = std::max(scratch_elems, (size_t)ps.two.nslot * (size_t)ps.L * 16);
+      ctrl_words = std::max(ctrl_words, 1 + 2 * ps.two.nslot);
+    }
+  if (scratch_elems) {
+    if (int rc = P->scratch.alloc(scratch_elems * 8)) return rc;
+    if (int rc = P->ctrl.alloc((size_t)ctrl_words * sizeof(unsigned))) return rc;
+    for (Pass& ps : P->passes)
+      if (ps.kind == K_TWO) {
+        ps.two.scratch = (float2*)P->scratch.p;
+        ps.two.ctrl = (unsigned*)P->ctrl.p;
+      }
+  }
   const uint64_t elems = P->is2d ? P->ny * P->nx * P->batch : P->n * P->batch;
   if (need_work) {
     int rc = P->work.alloc(elems * sizeof(tfb::C2<Real>));
@@ -493,7 +596,10 @@ int exec_impl(tilefft_plan_s* P, const void* in, void* out, int sign, cudaStream
   const uint64_t total = P->is2d ? P->ny * P->nx : P->n;
   const Real scale = inv ? (Real)1 / (Real)total : (Real)1;
   auto buf = [&](int id) -> void* { return id == 0 ? const_cast<void*>(in) : id == 1 ? out : P->work.p; };
-  for (const Pass& ps : P->passes) {
+  // two-level passes stream their input with TMA (16-byte aligned); an
+  // unaligned user buffer takes the equivalent plan without them
+  const bool use_alt = !P->passes_alt.empty() && ((uintptr_t)in % 16 != 0);
+  for (const Pass& ps : use_alt ? P->passes_alt : P->passes) {
     int rc;
     const void* src = buf(ps.src);
     void* dst = buf(ps.dst);
@@ -645,8 +751,21 @@ int tilefft_plan_create_2d(tilefft_plan_t* out, uint64_t ny, uint64_t nx, uint64
     rows.dst = multi ? 2 : 1;
     rows.nrows = (long long)(ny * batch);
     rows.tw_off = add_stage_table(tb, (int)nx);
+    // 2048..8192-point columns (fp32): one two-level pass through L2
+    const bool two = std::is_same<Real, float>::value && two_level_enabled() && two_level_len(ny) && nx % 16 == 0;
+    if (two) rows.dst = 2;
     P->passes.push_back(rows);
     P->dev_factors.push_back(nx);
+    if (two) {
+      Pass c = make_two_pass(P, tb, ny, (long long)nx, (long long)nx, (long long)batch, (long long)(ny * nx),
+                             (long long)(ny * nx), (long long)nx, 0, false, 0);
+      c.src = 2;
+      c.dst = 1;
+      c.final_pass = true;
+      P->passes.push_back(c);
+      P->dev_factors.push_back(ny);
+      return finish_plan<Real>(P, tb);
+    }
     int rc = build_axis_passes<Real>(P, tb, ny, nx, batch, multi ? 2 : 1, 1);
     if (rc) return rc;
     return finish_plan<Real>(P, tb);

@@ -1,0 +1,310 @@
+// Two-level pass (fp32): one HBM read + one HBM write of an L = LA * LB point
+// FFT along a strided axis, for L too long for one CTA's shared memory
+// (8192-point columns of 2^26 = 8192 x 8192 and of the 8192^2 image).
+//
+// The reference's pass (tiled_fft.hpp:229-310) keeps a whole comb in fast
+// memory. A 16-comb tile of 8192 points is 1 MB, far beyond one SM, so the
+// comb is split once more (n = n1 + LB n2, k = k2 + LA k1):
+//
+//   A item (group g, n1):   LA-point FFT over n2 of 16 adjacent combs
+//                           (TMA tile in, Stockham in registers + padded
+//                           shared memory), times W_L^{n1 k2}, written to a
+//                           per-group scratch slot that lives in L2;
+//   B item (group g, kb):   LB-point DFT over n1 for a block of k2 (scratch
+//                           read from L2), optional inter-pass root
+//                           W_M^{c k} (tiled_fft.hpp:284-294), stored to HBM.
+//
+// Only the A loads and the B stores touch HBM; the scratch round trip stays
+// in the 126 MB L2 (a bounded ring of slots, each line discarded from L2
+// once consumed so dirty scratch is never written back). The kernel is
+// persistent: CTAs take items from a global counter in an order in which
+// every dependency (B(g) on the A items of g, A(g) on the slot's previous
+// B items) was handed out earlier, so spinning on it cannot deadlock.
+//
+// OUTT = 0: output along the same comb (out[c + k * es_out]).
+// OUTT = 1: output transposed, row c of a [cols][L] matrix (out[c * L + k]):
+//           the four-step pass 1 whose result pass 2 reads as combs.
+#pragma once
+#include "fast_kernels.cuh"
+
+namespace tfb {
+
+struct TwoArgs {
+  long long groups;          // batch * chunks
+  long long chunks;          // 16-column chunks per batch item
+  long long bs_in, bs_out;   // batch strides (elements)
+  long long es_out;          // OUTT=0: output element stride along the axis; OUTT=1: output row pitch
+  int D;                     // lag between A(g) and B(g) in the hand-out order (groups)
+  int nslot;                 // scratch slots (> D)
+  int discard;               // discard consumed scratch lines from L2
+  int fb;                    // fine-table bits of the inter-pass root tables
+  uint32_t m_mask;           // M - 1 (inter-pass root W_M)
+  float2* scratch;           // nslot * L * 16 elements
+  unsigned* ctrl;            // [0] work counter, [1..nslot] A done, [nslot+1..2 nslot] B done
+};
+
+template <int LA, int LB, bool INV, int OUTT>
+struct TwoCfg {
+  using V = float2;
+  static constexpr int F = 16;
+  static constexpr int L = LA * LB;
+  using Sh = Shape<LA, 32>;
+  static constexpr int T = Sh::T;               // threads per LA-point FFT
+  static constexpr int THREADS = F * T;
+  static_assert(THREADS == 256, "two-level pass expects 256 threads (LA = 512)");
+  static constexpr int KB = LA / LB;            // k2 values per B item
+  static constexpr int PAIRS = KB * F / THREADS;  // (k2, comb) pairs per thread in a B item
+  static_assert(PAIRS >= 1 && PAIRS * THREADS == KB * F, "B item must tile the CTA");
+  static_assert(OUTT == 0 || KB % 32 == 0, "transposed B items need 32 consecutive k2 per warp");
+  static constexpr int TILE = LA * F;           // elements per A tile
+  static constexpr int TILE_BYTES = TILE * 8;
+  static constexpr int NR = 2;                  // exchange rounds (half the combs per round)
+  static constexpr int FX = F / NR;
+  static constexpr int REG = RegionPad<LA, T>::v;  // OUTT=1: per-FFT exchange region
+  static constexpr int XB = OUTT == 0 ? LA * FX : FX * REG;
+  static constexpr int BL = LA < 256 ? LA : 256;  // TMA box rows
+  static constexpr int SMEM = TILE_BYTES + XB * 8 + 16 + 1024;  // + mbarrier + 1024-B alignment slack
+  static constexpr int GROUP = L * F;           // scratch elements per group
+};
+
+__device__ __forceinline__ void tma_load_4d_l2(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                               uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_geq(const unsigned* p, unsigned v) {
+  while (ld_acquire_u32(p) < v) __nanosleep(40);
+}
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+// Item hand-out order: supersteps j = 0 .. G + D - 1, superstep j holds the
+// LB A items of group j (if j < G) followed by the LB B items of group j - D
+// (if j >= D). Returns kind 0 = A, 1 = B, -1 = done.
+__device__ __forceinline__ int two_decode(long long id, long long G, int D, int LBv, long long& g, int& sub) {
+  const long long p1 = (long long)D * LBv;
+  if (id < p1) { g = id / LBv; sub = (int)(id % LBv); return 0; }
+  id -= p1;
+  const long long mid = (G - D) * 2 * LBv;
+  if (id < mid) {
+    const long long j = D + id / (2 * LBv);
+    const int p = (int)(id % (2 * LBv));
+    if (p < LBv) { g = j; sub = p; return 0; }
+    g = j - D; sub = p - LBv; return 1;
+  }
+  id -= mid;
+  if (id < p1) { g = G - D + id / LBv; sub = (int)(id % LBv); return 1; }
+  return -1;
+}
+
+// Tensor map (4-D, 8-byte elements): {column, n1 (stride es), n2 (stride LB*es), batch}.
+// OUTT=1 tiles are loaded with the 128-byte swizzle: element (n2, f) lives at
+// row n2, 16-byte chunk (f/2) ^ (n2 & 7).
+template <int LA, int LB, bool INV, int OUTT, bool TWID>
+__global__ void __launch_bounds__(256, 2)
+k_two(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, TwoArgs a, const float2* __restrict__ tw,
+      const float2* __restrict__ twl, const double2* __restrict__ wc, const double2* __restrict__ wf, float scale) {
+  using Cfg = TwoCfg<LA, LB, INV, OUTT>;
+  using V = float2;
+  using Sh = typename Cfg::Sh;
+  constexpr int F = Cfg::F, T = Cfg::T, KB = Cfg::KB;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  V* tile = reinterpret_cast<V*>(base);
+  V* xb = tile + Cfg::TILE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(xb + Cfg::XB);
+  const int tid = threadIdx.x;
+  const long long G = a.groups;
+  const int D = a.D;
+  unsigned* doneA = a.ctrl + 1;
+  unsigned* doneB = a.ctrl + 1 + a.nslot;
+  __shared__ long long s_next_g;
+  __shared__ int s_next_kind, s_next_sub;
+  unsigned* work = a.ctrl;
+
+  if (tid == 0) {
+    mbar_init(full, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](long long g, int n1) {
+    const long long b = g / a.chunks, ch = g % a.chunks;
+    mbar_arrive_expect_tx(full, Cfg::TILE_BYTES);
+#pragma unroll 1
+    for (int r = 0; r < LA; r += Cfg::BL)
+      tma_load_4d_l2(tile + r * F, &tmap, (int)(ch * F), n1, r, (int)b, full);
+  };
+  // take the next item from the global counter; if it is an A item, start
+  // its tile load right away (the tile is free whenever this is called)
+  auto grab = [&]() {
+    long long g = 0;
+    int sub = 0;
+    const long long id = (long long)atomicAdd(work, 1u);
+    const int kind = two_decode(id, G, D, LB, g, sub);
+    if (kind == 0) issue(g, sub);
+    s_next_g = g;
+    s_next_kind = kind;
+    s_next_sub = sub;
+  };
+
+  if (tid == 0) grab();
+  __syncthreads();
+  long long g = s_next_g;
+  int kind = s_next_kind, sub = s_next_sub;
+  uint32_t phase = 0;
+
+#pragma unroll 1
+  while (kind >= 0) {
+    const int slot = (int)(g % a.nslot);
+    const unsigned gen = (unsigned)(g / a.nslot);
+    V* scr = reinterpret_cast<V*>(a.scratch) + (size_t)slot * Cfg::GROUP;
+    if (kind == 0) {
+      // ------------------------------------------------------------ A item
+      const int n1 = sub;
+      mbar_wait(full, phase);
+      phase ^= 1;
+      V v[Sh::R];
+      int t, f;
+      if constexpr (OUTT == 0) {
+        f = tid % F;
+        t = tid / F;
+#pragma unroll
+        for (int q = 0; q < Sh::R; ++q) v[q] = tile[(t + q * T) * F + f];
+      } else {
+        f = tid / T;
+        t = tid % T;
+#pragma unroll
+        for (int q = 0; q < Sh::R; ++q) {
+          const int n2 = t + q * T;
+          v[q] = tile[n2 * F + ((((f >> 1) ^ (n2 & 7))) << 1) + (f & 1)];
+        }
+      }
+      const int my_round = f / Cfg::FX, fx = f % Cfg::FX;
+      fence_proxy_async_smem();
+      __syncthreads();  // tile consumed
+      if (tid == 0) grab();
+      SyncBlock sy;
+      if constexpr (OUTT == 0) {
+        auto ex = [xb, fx](int i) -> V& { return xb[i * Cfg::FX + fx]; };
+        Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
+      } else {
+        V* reg = xb + fx * Cfg::REG;
+        auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
+        Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
+      }
+      // W_L^{n1 k2}
+#pragma unroll
+      for (int j = 0; j < Sh::R; ++j) {
+        const int k2 = out_index<LA, 32>(t, j);
+        v[j] = ctw<INV>(v[j], __ldg(twl + n1 * k2));
+      }
+      // the slot's previous group must be fully consumed
+      if (tid == 0 && gen > 0) wait_geq(doneB + slot, gen * LB);
+      __syncthreads();
+      if constexpr (OUTT == 0) {
+#pragma unroll
+        for (int j = 0; j < Sh::R; ++j) scr[((size_t)n1 * LA + out_index<LA, 32>(t, j)) * F + f] = v[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < Sh::R; ++j) scr[((size_t)n1 * F + f) * LA + out_index<LA, 32>(t, j)] = v[j];
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(doneA + slot, 1u);
+      }
+    } else {
+      // ------------------------------------------------------------ B item
+      const int kb = sub;
+      if (tid == 0) {
+        grab();
+        wait_geq(doneA + slot, (gen + 1) * LB);
+      }
+      __syncthreads();
+      const long long b = g / a.chunks, ch = g % a.chunks;
+#pragma unroll
+      for (int m = 0; m < Cfg::PAIRS; ++m) {
+        // pair p = (k2l, f): lanes run along f (OUTT=0) or along k2 (OUTT=1)
+        const int p = tid + 256 * m;
+        int f, k2l;
+        if constexpr (OUTT == 0) {
+          f = p % F;
+          k2l = p / F;
+        } else {
+          k2l = p % KB;
+          f = p / KB;
+        }
+        const int k2 = kb * KB + k2l;
+        V v[LB];
+#pragma unroll
+        for (int n1 = 0; n1 < LB; ++n1) {
+          const V* q = OUTT == 0 ? scr + ((size_t)n1 * LA + k2) * F + f : scr + ((size_t)n1 * F + f) * LA + k2;
+          v[n1] = __ldcg(q);
+        }
+        reg_dft<LB, INV>(v);
+        const long long c = ch * F + f;  // column (comb) index
+        if constexpr (TWID) {
+          // W_M^{c (k2 + LA k1)} = W^{c k2} * (W^{c LA})^{k1}, powers in fp64
+          double2 w = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)k2) & a.m_mask, a.fb);
+          const double2 st = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)LA) & a.m_mask, a.fb);
+#pragma unroll
+          for (int k1 = 0; k1 < LB; ++k1) {
+            v[k1] = ctw<INV>(v[k1], make_float2((float)w.x, (float)w.y));
+            if (k1 + 1 < LB) w = cmul(w, st);
+          }
+        }
+        if (scale != 1.0f) {
+#pragma unroll
+          for (int k1 = 0; k1 < LB; ++k1) v[k1] = mk(v[k1].x * scale, v[k1].y * scale);
+        }
+        if constexpr (OUTT == 0) {
+          V* o = out + b * a.bs_out + c;
+#pragma unroll
+          for (int k1 = 0; k1 < LB; ++k1) o[(long long)(k2 + LA * k1) * a.es_out] = v[k1];
+        } else {
+          V* o = out + b * a.bs_out + c * a.es_out + k2;
+#pragma unroll
+          for (int k1 = 0; k1 < LB; ++k1) o[LA * k1] = v[k1];
+        }
+      }
+      __syncthreads();  // all scratch reads of this item done
+      if (a.discard) {
+        // this item owns LB x KB x 16 elements = LB*KB*F*8/128 lines
+        constexpr int LINES = LB * KB * F * 8 / 128;
+        for (int i = tid; i < LINES; i += 256) {
+          const V* q;
+          if constexpr (OUTT == 0) {
+            const int n1 = i / KB, k2 = kb * KB + i % KB;  // one line = 16 combs of (n1, k2)
+            q = scr + ((size_t)n1 * LA + k2) * F;
+          } else {
+            constexpr int LPR = KB * 8 / 128;               // lines per (n1, f) row segment
+            const int row = i / LPR, part = i % LPR;        // row = n1 * F + f
+            q = scr + (size_t)row * LA + kb * KB + part * 16;
+          }
+          discard_l2(q);
+        }
+        __syncthreads();
+      }
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(doneB + slot, 1u);
+      }
+    }
+    __syncthreads();
+    g = s_next_g;
+    kind = s_next_kind;
+    sub = s_next_sub;
+  }
+}
+
+}  // namespace tfb
