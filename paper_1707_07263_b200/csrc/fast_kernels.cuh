@@ -403,24 +403,27 @@ __device__ __forceinline__ long long final_index_dev(const CombArgs& a, long lon
 // Combs per CTA: one 128-byte line per comb step (16 fp32 / 8 fp64 elements).
 template <typename Real> struct FOf { static constexpr int v = 128 / (int)sizeof(C2<Real>); };
 
-template <typename Real, int L>
+// F < 16 (small transforms whose data sits in L2: more, smaller tiles so
+// every SM gets work) pads the exchange by one element per 32 / F rows.
+template <typename Real, int L, int F_ = FOf<Real>::v>
 struct CombCfg {
   using V = C2<Real>;
   static constexpr int RMAX = RmaxOf<Real>::v;
   using Sh = Shape<L, RMAX>;
-  static constexpr int F = FOf<Real>::v;
+  static constexpr int F = F_;
+  static constexpr bool PAD = F < FOf<Real>::v;
   static constexpr int THREADS = F * Sh::T;
-  static constexpr int SMEM = (Sh::NST > 1 ? L * F : 1) * (int)sizeof(V);
+  static constexpr int SMEM = (Sh::NST > 1 ? L * F + (PAD ? L * F / 32 : 0) : 1) * (int)sizeof(V);
   // two resident CTAs per SM (<= 128 registers at 256 threads) so one CTA's
   // loads overlap the other's butterflies
   static constexpr int MINB = THREADS <= 256 ? 2 : 1;
 };
 
-template <typename Real, int L, bool INV, bool TWID, int MODE>
-__global__ void __launch_bounds__(CombCfg<Real, L>::THREADS, CombCfg<Real, L>::MINB)
+template <typename Real, int L, bool INV, bool TWID, int MODE, int F_ = FOf<Real>::v>
+__global__ void __launch_bounds__(CombCfg<Real, L, F_>::THREADS, CombCfg<Real, L, F_>::MINB)
 k_comb(const C2<Real>* in, C2<Real>* out, CombArgs a, const C2<Real>* __restrict__ tw,
        const double2* __restrict__ wc, const double2* __restrict__ wf, Real scale) {
-  using Cfg = CombCfg<Real, L>;
+  using Cfg = CombCfg<Real, L, F_>;
   using V = C2<Real>;
   using Sh = typename Cfg::Sh;
   constexpr int F = Cfg::F;
@@ -457,7 +460,10 @@ k_comb(const C2<Real>* in, C2<Real>* out, CombArgs a, const C2<Real>* __restrict
   V v[Sh::R];
 #pragma unroll
   for (int q = 0; q < Sh::R; ++q) v[q] = in[in_base + fl + (long long)(t + q * Sh::T) * s_in];
-  auto ex = [sm, f](int i) -> V& { return sm[i * F + f]; };
+  auto ex = [sm, f](int i) -> V& {
+    if constexpr (Cfg::PAD) return sm[i * F + f + ((i * F) >> 5)];
+    else return sm[i * F + f];
+  };
   SyncBlock s;
   Stages<V, L, Cfg::RMAX, INV, 0>::run(v, t, ex, tw, s);
   if constexpr (TWID) interpass_scale<V, L, Cfg::RMAX, INV>(v, t, r, a.m_mask, a.fb, wc, wf);
@@ -660,12 +666,12 @@ struct FinalArgs {
   long long out_w[8], sub_w[8];
 };
 
-template <typename Real, int L>
+template <typename Real, int L, int F_ = FOf<Real>::v>
 struct FinalCfg {
   using V = C2<Real>;
   static constexpr int RMAX = RmaxOf<Real>::v;
   using Sh = Shape<L, RMAX>;
-  static constexpr int F = FOf<Real>::v;
+  static constexpr int F = F_;
   static constexpr int THREADS = F * Sh::T;
   // FFT regions == T (mod 16) and a transpose row stride F + 16/T: every
   // half-warp access (several FFTs per half-warp when T < 16) is conflict free
@@ -675,10 +681,10 @@ struct FinalCfg {
   static constexpr int SMEM = (A > B ? A : B) * (int)sizeof(V);
 };
 
-template <typename Real, int L, bool INV>
-__global__ void __launch_bounds__(FinalCfg<Real, L>::THREADS)
+template <typename Real, int L, bool INV, int F_ = FOf<Real>::v>
+__global__ void __launch_bounds__(FinalCfg<Real, L, F_>::THREADS)
 k_final_t(const C2<Real>* in, C2<Real>* out, FinalArgs a, const C2<Real>* __restrict__ tw, Real scale) {
-  using Cfg = FinalCfg<Real, L>;
+  using Cfg = FinalCfg<Real, L, F_>;
   using V = C2<Real>;
   using Sh = typename Cfg::Sh;
   constexpr int F = Cfg::F;

@@ -10,6 +10,19 @@
 
 namespace tfb_host {
 
+inline bool env_set(const char* name) {
+  const char* e = std::getenv(name);
+  return e && *e && *e != '0';
+}
+
+inline int sm_count() {
+  static int n[16] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!n[dev & 15]) cudaDeviceGetAttribute(&n[dev & 15], cudaDevAttrMultiProcessorCount, dev);
+  return n[dev & 15];
+}
+
 // FFTs per CTA for K_ROWS: 8 warps of work for L <= 1024 (fp32), one FFT per CTA above.
 template <typename Real>
 constexpr int rows_fpc(int L) {
@@ -85,13 +98,6 @@ inline bool comb_w_disabled() {
   return !(e && *e && *e != '0');
 }
 
-inline int sm_count() {
-  static int n[16] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!n[dev & 15]) cudaDeviceGetAttribute(&n[dev & 15], cudaDevAttrMultiProcessorCount, dev);
-  return n[dev & 15];
-}
 
 // Strided comb tile as a 4-D tensor {column (8-byte words), n, rr, group}.
 template <typename Real, int L>
@@ -217,6 +223,26 @@ int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, const
   using V = tfb::C2<Real>;
   const V* t = (const V*)tb;
   const double2* t64 = (const double2*)tb64;
+  // small 1D transforms (data in L2, fewer 16-comb tiles than 2 per SM):
+  // 4-comb tiles spread the pass over every SM
+  if constexpr (std::is_same<Real, float>::value && L >= 64) {
+    constexpr int FS = 4;
+    if (ps.kind == K_COMB1D && ps.comb.ntiles < 2LL * sm_count() && ps.comb.rps % 16 == 0 && !env_set("TILEFFT_NO_SMALLF")) {
+      using CfgS = tfb::CombCfg<float, L, FS>;
+      tfb::CombArgs a = ps.comb;
+      a.chunks *= 16 / FS;
+      a.ntiles *= 16 / FS;
+      a.fvalid = FS;
+      auto k = tfb::k_comb<float, L, INV, true, 0, FS>;
+      if (int rc = ensure_smem((const void*)k, CfgS::SMEM)) return rc;
+      k<<<(unsigned)a.ntiles, CfgS::THREADS, CfgS::SMEM, st>>>((const float2*)in, (float2*)out, a,
+                                                              (const float2*)tb + ps.tw_off,
+                                                              (const double2*)tb64 + ps.wc_off,
+                                                              (const double2*)tb64 + ps.wf_off, (float)scale);
+      CUDA_TRY(cudaGetLastError());
+      return 0;
+    }
+  }
   if constexpr (tfb::Shape<L, tfb::RmaxOf<Real>::v>::NST > 1) {
     CUtensorMap map;
     // TMA pipelining pays off on the long 1D comb passes (2^30: 13.3 -> 11.8 ms);
@@ -273,8 +299,23 @@ int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, const
 template <typename Real, int L, bool INV>
 int launch_final(const Pass& ps, const void* in, void* out, const void* tb, const void*, Real scale,
                  cudaStream_t st) {
-  using Cfg = tfb::FinalCfg<Real, L>;
   using V = tfb::C2<Real>;
+  if constexpr (std::is_same<Real, float>::value && L >= 64) {
+    constexpr int FS = 4;
+    if (ps.fin.ntiles < 2LL * sm_count() && !env_set("TILEFFT_NO_SMALLF")) {
+      using CfgS = tfb::FinalCfg<float, L, FS>;
+      tfb::FinalArgs a = ps.fin;
+      a.chunks *= 16 / FS;
+      a.ntiles *= 16 / FS;
+      auto k = tfb::k_final_t<float, L, INV, FS>;
+      if (int rc = ensure_smem((const void*)k, CfgS::SMEM)) return rc;
+      k<<<(unsigned)a.ntiles, CfgS::THREADS, CfgS::SMEM, st>>>((const float2*)in, (float2*)out, a,
+                                                              (const float2*)tb + ps.tw_off, (float)scale);
+      CUDA_TRY(cudaGetLastError());
+      return 0;
+    }
+  }
+  using Cfg = tfb::FinalCfg<Real, L>;
   auto k = tfb::k_final_t<Real, L, INV>;
   if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
   k<<<(unsigned)ps.grid, Cfg::THREADS, Cfg::SMEM, st>>>((const V*)in, (V*)out, ps.fin, (const V*)tb + ps.tw_off,

@@ -132,6 +132,19 @@ struct tilefft_plan_s {
   DevBuf work;            // workspace (batch * n elements)
   std::vector<Pass> passes_alt;  // same transform without two-level passes (used when the input is not 16-B aligned)
   DevBuf scratch, ctrl;   // two-level passes: L2-resident exchange slots and their counters
+  // Replayed launch sequences: one CUDA graph per (in, out, sign), captured on
+  // first use; a replay costs one cudaGraphLaunch instead of per-pass host work
+  // (tensor-map encoding, occupancy queries, 2-3 launches).
+  struct GraphEntry {
+    const void* in;
+    void* out;
+    int sign;
+    cudaGraphExec_t exec;
+  };
+  static constexpr size_t kMaxGraphs = 8;
+  std::vector<GraphEntry> graphs;
+  std::mutex graph_mu;
+  cudaStream_t cap_stream = nullptr;
   size_t table_elems = 0;
   // host-path staging
   std::mutex host_mu;
@@ -151,6 +164,8 @@ struct tilefft_plan_s {
   tilefft_plan_s* inner = nullptr;  // row FFTs of length n2 over the rank's n1/nranks rows
   ~tilefft_plan_s() {
     if (inner) tilefft_plan_destroy(inner);
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     for (int i = 0; i < kHostStreams; ++i) {
       if (hs[i]) cudaStreamDestroy(hs[i]);
       if (hev[i]) cudaEventDestroy(hev[i]);
@@ -789,7 +804,39 @@ int tilefft_exec_c2c(tilefft_plan_t P, const void* in, void* out, int sign, void
     return fail(TILEFFT_EINVAL, "tilefft_exec_c2c: permute mode is forward only");
   CUDA_TRY(cudaSetDevice(P->device));
   cudaStream_t st = (cudaStream_t)stream;
-  return P->elem_bytes == 8 ? exec_impl<float>(P, in, out, sign, st) : exec_impl<double>(P, in, out, sign, st);
+  auto direct = [&](cudaStream_t s) {
+    return P->elem_bytes == 8 ? exec_impl<float>(P, in, out, sign, s) : exec_impl<double>(P, in, out, sign, s);
+  };
+  if (env_flag("TILEFFT_NO_GRAPH")) return direct(st);
+  std::lock_guard<std::mutex> lock(P->graph_mu);
+  for (auto& g : P->graphs)
+    if (g.in == in && g.out == out && g.sign == sign) {
+      CUDA_TRY(cudaGraphLaunch(g.exec, st));
+      return 0;
+    }
+  // capture the pass sequence once on a private stream (the caller's stream
+  // may be the legacy default stream, which cannot be captured)
+  if (!P->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&P->cap_stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamBeginCapture(P->cap_stream, cudaStreamCaptureModeThreadLocal));
+  const int rc = direct(P->cap_stream);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(P->cap_stream, &graph);
+  if (rc) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (ce != cudaSuccess) return fail(TILEFFT_ECUDA, "stream capture failed: %s", cudaGetErrorString(ce));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) return fail(TILEFFT_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ie));
+  if (P->graphs.size() >= tilefft_plan_s::kMaxGraphs) {
+    cudaGraphExecDestroy(P->graphs.front().exec);
+    P->graphs.erase(P->graphs.begin());
+  }
+  P->graphs.push_back({in, out, sign, exec});
+  CUDA_TRY(cudaGraphLaunch(exec, st));
+  return 0;
 }
 
 int tilefft_exec_c2c_host(tilefft_plan_t P, const void* h_in, void* h_out, int sign) {
