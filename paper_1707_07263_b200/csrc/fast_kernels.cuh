@@ -528,6 +528,7 @@ struct CombTmaArgs {
   // offset `col_off`) — the all-to-all transpose fused into the store.
   long long r_off, pitch, col_off;
   int rows_per_rank, nranks;
+  int copy_only;            // diagnostics: 1 = skip the butterflies, 2 = skip the inter-pass roots
   void* peers[16];
 };
 
@@ -629,8 +630,11 @@ k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs 
     }
     auto ex = [xb, fx](int i) -> V& { return xb[i * Cfg::FX + fx]; };
     SyncBlock sy;
-    Stages<V, L, Cfg::RMAX, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
-    if constexpr (TWID) interpass_scale<V, L, Cfg::RMAX, INV>(v, t, r, a.m_mask, a.fb, wc, wf);
+    if (a.copy_only != 1) {
+      Stages<V, L, Cfg::RMAX, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
+      if constexpr (TWID)
+        if (a.copy_only != 2) interpass_scale<V, L, Cfg::RMAX, INV>(v, t, r, a.m_mask, a.fb, wc, wf);
+    }
     if (f < a.fvalid) {
 #pragma unroll
       for (int j = 0; j < Sh::R; ++j) {

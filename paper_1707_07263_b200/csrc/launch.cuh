@@ -264,6 +264,7 @@ int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, const
       a.fb = c.fb;
       a.p = c.p;
       a.m_mask = c.m_mask;
+      if (const char* e = std::getenv("TILEFFT_DEBUG_COPYONLY")) a.copy_only = std::atoi(e);
       for (int i = 0; i < 8; ++i) {
         a.out_w[i] = c.out_w[i];
         a.sub_w[i] = c.sub_w[i];

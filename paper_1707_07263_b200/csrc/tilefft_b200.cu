@@ -359,7 +359,20 @@ int build_fast_1d(tilefft_plan_s* P, TableBuilder<Real>& tb) {
     P->dev_factors = {n};
     return 0;
   }
-  const std::vector<uint64_t> f = balanced_factors(n, 1024);
+  std::vector<uint64_t> f = balanced_factors(n, 1024);
+  if (const char* e = std::getenv("TILEFFT_FAST_FACTORS")) {  // tuning: explicit pass lengths, e.g. "512,256,512"
+    std::vector<uint64_t> o;
+    uint64_t prod = 1;
+    for (const char* c = e; *c;) {
+      const uint64_t v = std::strtoull(c, const_cast<char**>(&c), 10);
+      if (v) { o.push_back(v); prod *= v; }
+      while (*c == ',') ++c;
+      if (!v) break;
+    }
+    bool ok = prod == n && !o.empty();
+    for (uint64_t v : o) ok = ok && is_pow2(v) && v >= 2 && v <= 1024;
+    if (ok) f = o;
+  }
   const Geo g = geometry(n, f);
   const size_t p = f.size();
   if (p > 8) return fail(TILEFFT_EINVAL, "transform too long for the fast path (%zu passes)", p);
