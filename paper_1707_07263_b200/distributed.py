@@ -115,20 +115,29 @@ class DistributedFFT:
         o = self.ops
         self.rows = o.alloc((o.r, o.n2))
         self._opened = []
+        self._it = 0
         if self.exchange == "local":
             o.set_dests([o.ptr(self.rows)], o.n2, 0)
         elif self.exchange == "p2p":
-            handles = [None] * self.world
-            self.dist.all_gather_object(handles, o.ipc_handle(self.rows))
-            ptrs = []
-            for g, h in enumerate(handles):
-                if g == self.rank:
-                    ptrs.append(o.ptr(self.rows))
-                else:
-                    p = o.ipc_open(h)
-                    self._opened.append(p)
-                    ptrs.append(p)
-            o.set_dests(ptrs, o.n2, self.rank * o.c)
+            # Two row slabs used alternately: a fast rank's pass 1 of call i+1
+            # writes the other slab, never the one a slower peer's pass 2 of
+            # call i may still be reading (the barrier of call i orders call
+            # i-1's pass 2 before every pass-1 store of call i+1).
+            self._slabs = [self.rows, o.alloc((o.r, o.n2))]
+            self._dests = []
+            for slab in self._slabs:
+                handles = [None] * self.world
+                self.dist.all_gather_object(handles, o.ipc_handle(slab))
+                ptrs = []
+                for g, h in enumerate(handles):
+                    if g == self.rank:
+                        ptrs.append(o.ptr(slab))
+                    else:
+                        p = o.ipc_open(h)
+                        self._opened.append(p)
+                        ptrs.append(p)
+                self._dests.append(ptrs)
+            o.set_dests(self._dests[0], o.n2, self.rank * o.c)
         elif self.exchange == "nccl":
             self.stage = o.alloc((self.world, o.r, o.c))
             self.recv = o.alloc((self.world, o.r, o.c))
@@ -142,6 +151,11 @@ class DistributedFFT:
         sign = _capi.INVERSE if inverse else _capi.FORWARD
         if out is None:
             out = o.alloc((o.r, o.n2))
+        if self.exchange == "p2p":
+            b = self._it & 1
+            self._it += 1
+            self.rows = self._slabs[b]
+            o.set_dests(self._dests[b], o.n2, self.rank * o.c)
         o.pass1(col_slab, sign)
         if self.exchange == "p2p":
             o.sync()              # this rank's peer stores are complete ...

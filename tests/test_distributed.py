@@ -70,6 +70,86 @@ class OracleOps:
         pass
 
 
+class SharedMemOracleOps(OracleOps):
+    """OracleOps whose row slabs live in shared-memory files, so the "p2p"
+    exchange (pass 1 storing straight into the peers' slabs, CUDA IPC on the
+    GPU) runs across processes on the CPU: ipc_handle = the file name."""
+
+    _count = 0
+
+    def alloc(self, shape):
+        import tempfile
+        import torch
+        SharedMemOracleOps._count += 1
+        fd, path = tempfile.mkstemp(prefix=f"tilefft_r{self.rank}_", dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+        os.close(fd)
+        nbytes = int(np.prod(shape)) * 16
+        t = torch.from_file(path, shared=True, size=nbytes // 8, dtype=torch.float64).view(torch.complex128).view(shape)
+        t.zero_()
+        t._tilefft_path = path
+        self.paths = getattr(self, "paths", []) + [path]
+        return t
+
+    def ipc_handle(self, t):
+        return (t._tilefft_path, tuple(t.shape))
+
+    def ipc_open(self, h):
+        import torch
+        path, shape = h
+        nbytes = int(np.prod(shape)) * 16
+        return torch.from_file(path, shared=True, size=nbytes // 8, dtype=torch.float64).view(torch.complex128)
+
+
+def _p2p_worker(rank, world, port, n, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, os.path.dirname(HERE))
+    from paper_1707_07263_b200.distributed import DistributedFFT, column_slab
+    sys.path.insert(0, HERE)
+    from oracle_lib import Oracle
+    O = Oracle()
+    ops = SharedMemOracleOps(n, world, rank)
+    d = DistributedFFT(n, exchange="p2p", ops=ops)
+    outs = []
+    for seed in (11, 12, 13):  # three calls: both slabs of the double buffer, then the first again
+        x = O.random_bench_signal(n, seed)
+        outs.append(d.forward(torch.from_numpy(column_slab(x, world, rank))).numpy().copy())
+    gathered = [None] * world
+    dist.all_gather_object(gathered, outs)
+    if rank == 0:
+        q.put(gathered)
+    dist.barrier()
+    for path in ops.paths:
+        os.unlink(path)
+    dist.destroy_process_group()
+
+
+def test_distributed_p2p_orchestration_gloo():
+    """Peer-store exchange across 2 processes: every call matches the oracle,
+    including back-to-back calls that alternate the two row slabs."""
+    import multiprocessing as mp
+    from paper_1707_07263_b200.distributed import assemble_output
+    sys.path.insert(0, HERE)
+    from oracle_lib import Oracle, rel_l2
+    n, world = 1 << 16, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    gathered = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    O = Oracle()
+    for call, seed in enumerate((11, 12, 13)):
+        got = assemble_output([gathered[r][call] for r in range(world)], n)
+        assert rel_l2(got, O.fft_tiled(O.random_bench_signal(n, seed))) < 1e-12, call
+
+
 def _worker(rank, world, port, n, q):
     import torch
     import torch.distributed as dist
