@@ -73,7 +73,9 @@ k_comb_w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtens
   using Sh = Shape<L, 32>;
   constexpr int F = Cfg::F, T = Cfg::T, S = Cfg::S, NCB = Cfg::NCB;
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // align by pointer arithmetic: an integer round trip would lose the shared
+  // address space and turn every tile access into a generic LD.E/ST.E
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   V* tiles = reinterpret_cast<V*>(base);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + S * Cfg::TILE_BYTES);
   uint64_t* done = full + S;

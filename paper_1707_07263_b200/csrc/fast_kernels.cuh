@@ -419,18 +419,17 @@ struct CombCfg {
   static constexpr int MINB = THREADS <= 256 ? 2 : 1;
 };
 
-template <typename Real, int L, bool INV, bool TWID, int MODE, int F_ = FOf<Real>::v>
-__global__ void __launch_bounds__(CombCfg<Real, L, F_>::THREADS, CombCfg<Real, L, F_>::MINB)
-k_comb(const C2<Real>* in, C2<Real>* out, CombArgs a, const C2<Real>* __restrict__ tw,
-       const double2* __restrict__ wc, const double2* __restrict__ wf, Real scale) {
+// One comb tile (the body of K_COMB; also run by the fused small-transform kernel).
+template <typename Real, int L, bool INV, bool TWID, int MODE, int F_>
+__device__ __forceinline__ void comb_tile(const C2<Real>* in, C2<Real>* out, const CombArgs& a,
+                                          const C2<Real>* __restrict__ tw, const double2* __restrict__ wc,
+                                          const double2* __restrict__ wf, Real scale, long long tile,
+                                          C2<Real>* sm) {
   using Cfg = CombCfg<Real, L, F_>;
   using V = C2<Real>;
   using Sh = typename Cfg::Sh;
   constexpr int F = Cfg::F;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* sm = reinterpret_cast<V*>(smem_raw);
   const int f = threadIdx.x % F, t = threadIdx.x / F;
-  const long long tile = blockIdx.x;
   const long long chunk = tile % a.chunks;
   const long long g = tile / a.chunks;
   const long long batch = g / a.groups_per_batch;
@@ -476,6 +475,15 @@ k_comb(const C2<Real>* in, C2<Real>* out, CombArgs a, const C2<Real>* __restrict
       out[out_base + f + (long long)k * s_out] = x;
     }
   }
+}
+
+template <typename Real, int L, bool INV, bool TWID, int MODE, int F_ = FOf<Real>::v>
+__global__ void __launch_bounds__(CombCfg<Real, L, F_>::THREADS, CombCfg<Real, L, F_>::MINB)
+k_comb(const C2<Real>* in, C2<Real>* out, CombArgs a, const C2<Real>* __restrict__ tw,
+       const double2* __restrict__ wc, const double2* __restrict__ wf, Real scale) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  comb_tile<Real, L, INV, TWID, MODE, F_>(in, out, a, tw, wc, wf, scale, blockIdx.x,
+                                          reinterpret_cast<C2<Real>*>(smem_raw));
 }
 
 // ------------------------------------------------------------------ K_COMB_TMA
@@ -685,18 +693,13 @@ struct FinalCfg {
   static constexpr int SMEM = (A > B ? A : B) * (int)sizeof(V);
 };
 
-template <typename Real, int L, bool INV, int F_ = FOf<Real>::v>
-__global__ void __launch_bounds__(FinalCfg<Real, L, F_>::THREADS)
-k_final_t(const C2<Real>* in, C2<Real>* out, FinalArgs a, const C2<Real>* __restrict__ tw, Real scale) {
+template <typename Real, int L, bool INV, int F_>
+__device__ __forceinline__ void final_tile(const C2<Real>* in, C2<Real>* out, const FinalArgs& a,
+                                           const C2<Real>* __restrict__ tw, Real scale, long long tile, C2<Real>* sm) {
   using Cfg = FinalCfg<Real, L, F_>;
   using V = C2<Real>;
   using Sh = typename Cfg::Sh;
   constexpr int F = Cfg::F;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* sm = reinterpret_cast<V*>(smem_raw);
-  const long long tile = blockIdx.x;
-  const long long per_batch = a.ntiles / 1;  // tiles already include batch
-  (void)per_batch;
   const long long tiles_per_batch = a.chunks * a.sw0;
   const long long batch = tile / tiles_per_batch;
   const long long rem = tile % tiles_per_batch;
@@ -739,6 +742,13 @@ k_final_t(const C2<Real>* in, C2<Real>* out, FinalArgs a, const C2<Real>* __rest
       out[ob + (long long)k * a.out_w_last] = x;
     }
   }
+}
+
+template <typename Real, int L, bool INV, int F_ = FOf<Real>::v>
+__global__ void __launch_bounds__(FinalCfg<Real, L, F_>::THREADS)
+k_final_t(const C2<Real>* in, C2<Real>* out, FinalArgs a, const C2<Real>* __restrict__ tw, Real scale) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  final_tile<Real, L, INV, F_>(in, out, a, tw, scale, blockIdx.x, reinterpret_cast<C2<Real>*>(smem_raw));
 }
 
 }  // namespace tfb

@@ -99,6 +99,12 @@ inline bool comb_w_disabled() {
 }
 
 
+// Two-level passes use the warp-specialised kernel unless TILEFFT_TWO_WS=0.
+inline bool two_ws_enabled() {
+  const char* e = std::getenv("TILEFFT_TWO_WS");
+  return !(e && *e == '0');
+}
+
 // Strided comb tile as a 4-D tensor {column (8-byte words), n, rr, group}.
 template <typename Real, int L>
 bool encode_comb_map(CUtensorMap* map, const Pass& ps, const void* in) {
@@ -347,6 +353,19 @@ int launch_two_k(const Pass& ps, const void* in, void* out, const void* tb, cons
           CU_TENSOR_MAP_INTERLEAVE_NONE, OUTT ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled failed for the two-level pass");
+  const float2* t = (const float2*)tb;
+  const double2* t64 = (const double2*)tb64;
+  if (two_ws_enabled()) {
+    // warp-specialised variant: one 512-thread CTA per SM (A team + B team)
+    using WCfg = tfb::TwoWsCfg<LA, LB, INV, OUTT>;
+    auto kw = tfb::k_two_ws<LA, LB, INV, OUTT, TWID>;
+    if (int rc = ensure_smem((const void*)kw, WCfg::SMEM)) return rc;
+    CUDA_TRY(cudaMemsetAsync(a.ctrl, 0, sizeof(unsigned) * (2 + 2 * a.nslot), st));
+    kw<<<sm_count(), 512, WCfg::SMEM, st>>>(map, (float2*)out, a, t + ps.tw_off, t + ps.twl_off, t64 + ps.wc_off,
+                                             t64 + ps.wf_off, scale);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
   auto k = tfb::k_two<LA, LB, INV, OUTT, TWID>;
   if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
   static int occ[16] = {0};
@@ -358,8 +377,6 @@ int launch_two_k(const Pass& ps, const void* in, void* out, const void* tb, cons
   }
   const int grid = sm_count() * occ[dev & 15];
   CUDA_TRY(cudaMemsetAsync(a.ctrl, 0, sizeof(unsigned) * (1 + 2 * a.nslot), st));
-  const float2* t = (const float2*)tb;
-  const double2* t64 = (const double2*)tb64;
   k<<<grid, 256, Cfg::SMEM, st>>>(map, (float2*)out, a, t + ps.tw_off, t + ps.twl_off, t64 + ps.wc_off,
                                   t64 + ps.wf_off, scale);
   CUDA_TRY(cudaGetLastError());
@@ -392,9 +409,75 @@ int launch_two(const Pass& ps, const void* in, void* out, const void* tb, const 
   return fail(TILEFFT_EINVAL, "internal: no two-level kernel for %d x %d", ps.la, ps.lb);
 }
 
+// K_SMALL2: both passes of a small 2-pass fp32 plan in one launch. Returns 1
+// (nothing launched) when the kernel does not fit an SM, so the caller runs
+// the two passes as separate kernels.
+template <int L1, int L2, bool INV>
+int launch_small2_k(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, float scale,
+                    cudaStream_t st) {
+  using Cfg = tfb::Small2Cfg<L1, L2>;
+  auto k = tfb::k_small2<L1, L2, INV>;
+  if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
+  static int occ[16] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!occ[dev & 15]) {
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev & 15], k, Cfg::THREADS, Cfg::SMEM));
+    if (occ[dev & 15] < 1) occ[dev & 15] = -1;
+  }
+  if (occ[dev & 15] < 1) return 1;
+  tfb::CombArgs a1 = ps.comb;
+  a1.chunks *= 16 / Cfg::F1;
+  a1.ntiles *= 16 / Cfg::F1;
+  a1.fvalid = Cfg::F1;
+  tfb::FinalArgs a2 = ps.fin;
+  a2.chunks *= 16 / Cfg::F2;
+  a2.ntiles *= 16 / Cfg::F2;
+  const long long want = std::max(a1.ntiles, a2.ntiles);
+  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(want, (long long)occ[dev & 15] * sm_count()));
+  k<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>((const float2*)in, (float2*)ps.work_p, (float2*)out, a1, a2,
+                                           (const float2*)tb + ps.tw_off, (const float2*)tb + ps.tw2_off,
+                                           (const double2*)tb64 + ps.wc_off, (const double2*)tb64 + ps.wf_off, scale,
+                                           (unsigned long long*)ps.gbar);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <bool INV>
+int launch_small2(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, float scale,
+                  cudaStream_t st) {
+  switch (ps.L * 10000 + ps.L2) {
+    case 128 * 10000 + 128: return launch_small2_k<128, 128, INV>(ps, in, out, tb, tb64, scale, st);
+    case 256 * 10000 + 128: return launch_small2_k<256, 128, INV>(ps, in, out, tb, tb64, scale, st);
+    case 256 * 10000 + 256: return launch_small2_k<256, 256, INV>(ps, in, out, tb, tb64, scale, st);
+    case 512 * 10000 + 256: return launch_small2_k<512, 256, INV>(ps, in, out, tb, tb64, scale, st);
+    case 512 * 10000 + 512: return launch_small2_k<512, 512, INV>(ps, in, out, tb, tb64, scale, st);
+    case 1024 * 10000 + 512: return launch_small2_k<1024, 512, INV>(ps, in, out, tb, tb64, scale, st);
+    case 1024 * 10000 + 1024: return launch_small2_k<1024, 1024, INV>(ps, in, out, tb, tb64, scale, st);
+  }
+  return 1;
+}
+
 template <typename Real, bool INV>
 int launch_fast(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, Real scale,
                 cudaStream_t st) {
+  if (ps.kind == K_SMALL2) {
+    if constexpr (std::is_same<Real, float>::value) {
+      const int rc = launch_small2<INV>(ps, in, out, tb, tb64, scale, st);
+      if (rc <= 0) return rc;
+    }
+    // no fused kernel for this shape: the same two passes as separate kernels
+    Pass p1 = ps, p2 = ps;
+    p1.kind = K_COMB1D;
+    p1.grid = ps.comb.ntiles;
+    p2.kind = K_FINALT;
+    p2.L = ps.L2;
+    p2.tw_off = ps.tw2_off;
+    p2.twid = false;
+    p2.grid = ps.fin.ntiles;
+    if (int rc = launch_fast<Real, INV>(p1, in, ps.work_p, tb, tb64, (Real)1, st)) return rc;
+    return launch_fast<Real, INV>(p2, ps.work_p, out, tb, tb64, scale, st);
+  }
 #define DISPATCH(FN, ...)                                                     \
   switch (ps.L) {                                                             \
     case 2: return FN<Real, 2, INV>(ps, in, out, tb, tb64, scale, st);              \

@@ -132,6 +132,7 @@ struct tilefft_plan_s {
   DevBuf work;            // workspace (batch * n elements)
   std::vector<Pass> passes_alt;  // same transform without two-level passes (used when the input is not 16-B aligned)
   DevBuf scratch, ctrl;   // two-level passes: L2-resident exchange slots and their counters
+  DevBuf gbar;            // K_SMALL2 tile counter + pass-1 done counter (64-bit, monotonic)
   // Replayed launch sequences: one CUDA graph per (in, out, sign), captured on
   // first use; a replay costs one cudaGraphLaunch instead of per-pass host work
   // (tensor-map encoding, occupancy queries, 2-3 launches).
@@ -420,7 +421,24 @@ int build_fast_1d(tilefft_plan_s* P, TableBuilder<Real>& tb) {
     P->passes.push_back(ps);
   }
   P->dev_factors = f;
-  build_two_1d<Real>(P, tb);
+  if (build_two_1d<Real>(P, tb)) return 0;
+  // small (L2-resident) 2-pass fp32 plans: both passes in one launch. Opt-in
+  // (TILEFFT_FUSE=1): measured one 2.05 us step slower than two launches at
+  // every size 2^14..2^20 (16.4 vs 14.4 us at 2^20) -- the grab / release /
+  // acquire round trips between the passes cost more than the launch gap.
+  if (std::is_same<Real, float>::value && p == 2 && n * B <= (1ull << 21) && f[1] >= 128 &&
+      (f[0] == f[1] || f[0] == 2 * f[1]) && env_flag("TILEFFT_FUSE")) {
+    Pass fused = P->passes[0];
+    const Pass& fin = P->passes[1];
+    fused.kind = K_SMALL2;
+    fused.src = 0;
+    fused.dst = 1;
+    fused.final_pass = true;
+    fused.fin = fin.fin;
+    fused.L2 = fin.L;
+    fused.tw2_off = fin.tw_off;
+    P->passes.assign(1, fused);
+  }
   return 0;
 }
 
@@ -581,14 +599,14 @@ template <typename Real>
 int finish_plan(tilefft_plan_s* P, TableBuilder<Real>& tb) {
   // workspace when any pass touches it
   bool need_work = false;
-  for (const Pass& ps : P->passes) need_work |= (ps.src == 2 || ps.dst == 2);
+  for (const Pass& ps : P->passes) need_work |= (ps.src == 2 || ps.dst == 2 || ps.kind == K_SMALL2);
   for (const Pass& ps : P->passes_alt) need_work |= (ps.src == 2 || ps.dst == 2);
   size_t scratch_elems = 0;
   int ctrl_words = 0;
   for (const Pass& ps : P->passes)
     if (ps.kind == K_TWO) {
       scratch_elems = std::max(scratch_elems, (size_t)ps.two.nslot * (size_t)ps.L * 16);
-      ctrl_words = std::max(ctrl_words, 1 + 2 * ps.two.nslot);
+      ctrl_words = std::max(ctrl_words, 2 + 2 * ps.two.nslot);
     }
   if (scratch_elems) {
     if (int rc = P->scratch.alloc(scratch_elems * 8)) return rc;
@@ -604,6 +622,15 @@ int finish_plan(tilefft_plan_s* P, TableBuilder<Real>& tb) {
     int rc = P->work.alloc(elems * sizeof(tfb::C2<Real>));
     if (rc) return rc;
   }
+  for (Pass& ps : P->passes)
+    if (ps.kind == K_SMALL2) {
+      if (!P->gbar.p) {
+        if (int rc = P->gbar.alloc(2 * sizeof(unsigned long long))) return rc;
+        CUDA_TRY(cudaMemset(P->gbar.p, 0, 2 * sizeof(unsigned long long)));
+      }
+      ps.work_p = P->work.p;
+      ps.gbar = (unsigned*)P->gbar.p;
+    }
   if (P->tb64 && !P->tb64->h.empty()) {
     int rc = P->tables64.alloc(P->tb64->h.size() * sizeof(double));
     if (rc) return rc;
@@ -1163,6 +1190,7 @@ int tilefft_plan_info(tilefft_plan_t P, tilefft_plan_info_t* info) {
   info->mode = P->mode;
   info->is_2d = P->is2d;
   info->passes = (uint32_t)P->passes.size();
+  for (const Pass& ps : P->passes) info->passes += ps.kind == K_SMALL2;  // two passes, one launch
   for (size_t i = 0; i < P->dev_factors.size() && i < 16; ++i) info->factors[i] = P->dev_factors[i];
   info->launches_per_exec = (uint32_t)P->passes.size();
   info->workspace_bytes = P->work.bytes;

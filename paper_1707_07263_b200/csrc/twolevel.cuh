@@ -43,7 +43,7 @@ struct TwoArgs {
   unsigned* ctrl;            // [0] work counter, [1..nslot] A done, [nslot+1..2 nslot] B done
 };
 
-template <int LA, int LB, bool INV, int OUTT>
+template <int LA, int LB, bool INV, int OUTT, int NR_ = 2>
 struct TwoCfg {
   using V = float2;
   static constexpr int F = 16;
@@ -58,7 +58,7 @@ struct TwoCfg {
   static_assert(OUTT == 0 || KB % 32 == 0, "transposed B items need 32 consecutive k2 per warp");
   static constexpr int TILE = LA * F;           // elements per A tile
   static constexpr int TILE_BYTES = TILE * 8;
-  static constexpr int NR = 2;                  // exchange rounds (half the combs per round)
+  static constexpr int NR = NR_;                // exchange rounds (1/NR of the combs per round)
   static constexpr int FX = F / NR;
   static constexpr int REG = RegionPad<LA, T>::v;  // OUTT=1: per-FFT exchange region
   static constexpr int XB = OUTT == 0 ? LA * FX : FX * REG;
@@ -75,13 +75,24 @@ __device__ __forceinline__ void tma_load_4d_l2(void* dst, const CUtensorMap* map
       : "memory");
 }
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+// Cross-CTA item protocol. An acquire load or a __threadfence() compiles to
+// CCTL.IVALL (invalidate the whole L1) on sm_100: done per poll it wipes the
+// L1-resident twiddle tables of every CTA on the SM. So the flag is polled
+// with relaxed loads and published with a release reduction (MEMBAR.GPU +
+// REDG, no L1 invalidate). The data it guards is only ever read with
+// L2-coherent loads (__ldcg = LDG.STRONG.GPU) after a barrier that depends on
+// the observed flag, and written only after the observed release of the
+// slot's previous readers, so no stale L1 line can be consumed.
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void wait_geq(const unsigned* p, unsigned v) {
-  while (ld_acquire_u32(p) < v) __nanosleep(40);
+  while (ld_relaxed_u32(p) < v) __nanosleep(40);
+}
+__device__ __forceinline__ void signal_release(unsigned* p) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
 }
 __device__ __forceinline__ void discard_l2(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
@@ -118,7 +129,9 @@ k_two(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, TwoArg
   using Sh = typename Cfg::Sh;
   constexpr int F = Cfg::F, T = Cfg::T, KB = Cfg::KB;
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // align by pointer arithmetic: an integer round trip would lose the shared
+  // address space and turn every tile access into a generic LD.E/ST.E
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   V* tile = reinterpret_cast<V*>(base);
   V* xb = tile + Cfg::TILE;
   uint64_t* full = reinterpret_cast<uint64_t*>(xb + Cfg::XB);
@@ -220,8 +233,7 @@ k_two(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, TwoArg
       }
       __syncthreads();
       if (tid == 0) {
-        __threadfence();
-        atomicAdd(doneA + slot, 1u);
+        signal_release(doneA + slot);
       }
     } else {
       // ------------------------------------------------------------ B item
@@ -296,14 +308,241 @@ k_two(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, TwoArg
         __syncthreads();
       }
       if (tid == 0) {
-        __threadfence();
-        atomicAdd(doneB + slot, 1u);
+        signal_release(doneB + slot);
       }
     }
     __syncthreads();
     g = s_next_g;
     kind = s_next_kind;
     sub = s_next_sub;
+  }
+}
+
+// ---------------------------------------------------------------- K_TWO_WS
+// Warp-specialised K_TWO: one persistent CTA per SM holds an A team (warps
+// 0-7) and a B team (warps 8-15) with their own item counters and named
+// barriers, so one team's waits (TMA tile, L2 round trip of the scratch,
+// the release fence after each item) overlap the other team's arithmetic
+// instead of stalling a CTA-wide __syncthreads. The A team streams its tiles
+// through a 2-slot TMA ring (the next tile loads while the current one is
+// transformed). Items are still handed out in group order, so the oldest
+// outstanding item of either kind only depends on older ones: with every CTA
+// resident (grid <= SMs), spinning cannot deadlock.
+//
+// ctrl: [0] A counter, [1..nslot] A done, [nslot+1..2 nslot] B done,
+//       [2 nslot + 1] B counter.
+template <int ID>
+struct SyncNamed {
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, 256;" ::"n"(ID) : "memory"); }
+};
+
+template <int LA, int LB, bool INV, int OUTT>
+struct TwoWsCfg {
+  // half-tile exchange buffer (2 rounds): a full one (1 round) leaves too little
+  // L1 for the twiddle tables and measured slower (618 vs 585 us, 8192^2)
+  using Base = TwoCfg<LA, LB, INV, OUTT, 2>;
+  static constexpr int NS = 2;  // A tile slots
+  static constexpr int SMEM = NS * Base::TILE_BYTES + Base::XB * 8 + NS * 8 + 1024;
+};
+
+template <int LA, int LB, bool INV, int OUTT, bool TWID>
+__global__ void __launch_bounds__(512, 1)
+k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, TwoArgs a, const float2* __restrict__ tw,
+         const float2* __restrict__ twl, const double2* __restrict__ wc, const double2* __restrict__ wf, float scale) {
+  using Cfg = typename TwoWsCfg<LA, LB, INV, OUTT>::Base;
+  constexpr int NS = TwoWsCfg<LA, LB, INV, OUTT>::NS;
+  using V = float2;
+  using Sh = typename Cfg::Sh;
+  constexpr int F = Cfg::F, T = Cfg::T, KB = Cfg::KB;
+  extern __shared__ unsigned char smem_raw[];
+  // align by pointer arithmetic: an integer round trip would lose the shared
+  // address space and turn every tile access into a generic LD.E/ST.E
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  V* tiles = reinterpret_cast<V*>(base);
+  V* xb = tiles + NS * Cfg::TILE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(xb + Cfg::XB);
+  __shared__ long long s_a_g[NS];
+  __shared__ int s_a_sub[NS];
+  __shared__ long long s_b_id;
+  const int team = threadIdx.x >> 8, tid = threadIdx.x & 255;
+  const long long G = a.groups;
+  const long long NA = G * LB;  // items of each kind
+  unsigned* doneA = a.ctrl + 1;
+  unsigned* doneB = a.ctrl + 1 + a.nslot;
+  unsigned* workA = a.ctrl;
+  unsigned* workB = a.ctrl + 1 + 2 * a.nslot;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (team == 0) {
+    // ============================================================ A team
+    SyncNamed<1> sy;
+    auto grab_into = [&](int s) {
+      const long long id = (long long)atomicAdd(workA, 1u);
+      if (id < NA) {
+        const long long g = id / LB;
+        const int n1 = (int)(id % LB);
+        const long long b = g / a.chunks, ch = g % a.chunks;
+        mbar_arrive_expect_tx(&full[s], Cfg::TILE_BYTES);
+#pragma unroll 1
+        for (int r = 0; r < LA; r += Cfg::BL)
+          tma_load_4d_l2(tiles + s * Cfg::TILE + r * F, &tmap, (int)(ch * F), n1, r, (int)b, &full[s]);
+        s_a_g[s] = g;
+        s_a_sub[s] = n1;
+      } else {
+        s_a_g[s] = -1;
+      }
+    };
+    if (tid == 0)
+      for (int s = 0; s < NS; ++s) grab_into(s);
+    sy();
+#pragma unroll 1
+    for (int k = 0;; ++k) {
+      const int s = k % NS;
+      const long long g = s_a_g[s];
+      const int n1 = s_a_sub[s];
+      if (g < 0) break;
+      const int slot = (int)(g % a.nslot);
+      const unsigned gen = (unsigned)(g / a.nslot);
+      V* scr = reinterpret_cast<V*>(a.scratch) + (size_t)slot * Cfg::GROUP;
+      mbar_wait(&full[s], (uint32_t)((k / NS) & 1));
+      const V* tile = tiles + s * Cfg::TILE;
+      V v[Sh::R];
+      int t, f;
+      if constexpr (OUTT == 0) {
+        f = tid % F;
+        t = tid / F;
+#pragma unroll
+        for (int q = 0; q < Sh::R; ++q) v[q] = tile[(t + q * T) * F + f];
+      } else {
+        f = tid / T;
+        t = tid % T;
+#pragma unroll
+        for (int q = 0; q < Sh::R; ++q) {
+          const int n2 = t + q * T;
+          v[q] = tile[n2 * F + ((((f >> 1) ^ (n2 & 7))) << 1) + (f & 1)];
+        }
+      }
+      const int my_round = f / Cfg::FX, fx = f % Cfg::FX;
+      fence_proxy_async_smem();
+      sy();  // slot s consumed (and s_a_* of slot s read by every thread)
+      if (tid == 0) grab_into(s);
+      if constexpr (OUTT == 0) {
+        auto ex = [xb, fx](int i) -> V& { return xb[i * Cfg::FX + fx]; };
+        Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
+      } else {
+        V* reg = xb + fx * Cfg::REG;
+        auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
+        Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
+      }
+#pragma unroll
+      for (int j = 0; j < Sh::R; ++j) {
+        const int k2 = out_index<LA, 32>(t, j);
+        v[j] = ctw<INV>(v[j], __ldg(twl + n1 * k2));
+      }
+      if (tid == 0 && gen > 0) wait_geq(doneB + slot, gen * LB);
+      sy();
+      if constexpr (OUTT == 0) {
+#pragma unroll
+        for (int j = 0; j < Sh::R; ++j) scr[((size_t)n1 * LA + out_index<LA, 32>(t, j)) * F + f] = v[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < Sh::R; ++j) scr[((size_t)n1 * F + f) * LA + out_index<LA, 32>(t, j)] = v[j];
+      }
+      sy();
+      if (tid == 0) {
+        signal_release(doneA + slot);
+      }
+    }
+  } else {
+    // ============================================================ B team
+    SyncNamed<2> sy;
+#pragma unroll 1
+    for (;;) {
+      if (tid == 0) {
+        const long long id = (long long)atomicAdd(workB, 1u);
+        s_b_id = id;
+        if (id < NA) {
+          const long long g = id / LB;
+          wait_geq(doneA + (int)(g % a.nslot), (unsigned)(g / a.nslot + 1) * LB);
+        }
+      }
+      sy();
+      const long long id = s_b_id;
+      if (id >= NA) break;
+      const long long g = id / LB;
+      const int kb = (int)(id % LB);
+      const int slot = (int)(g % a.nslot);
+      const V* scr = reinterpret_cast<const V*>(a.scratch) + (size_t)slot * Cfg::GROUP;
+      const long long b = g / a.chunks, ch = g % a.chunks;
+#pragma unroll
+      for (int m = 0; m < Cfg::PAIRS; ++m) {
+        const int p = tid + 256 * m;
+        int f, k2l;
+        if constexpr (OUTT == 0) {
+          f = p % F;
+          k2l = p / F;
+        } else {
+          k2l = p % KB;
+          f = p / KB;
+        }
+        const int k2 = kb * KB + k2l;
+        V v[LB];
+#pragma unroll
+        for (int n1 = 0; n1 < LB; ++n1) {
+          const V* q = OUTT == 0 ? scr + ((size_t)n1 * LA + k2) * F + f : scr + ((size_t)n1 * F + f) * LA + k2;
+          v[n1] = __ldcg(q);
+        }
+        reg_dft<LB, INV>(v);
+        const long long c = ch * F + f;
+        if constexpr (TWID) {
+          double2 w = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)k2) & a.m_mask, a.fb);
+          const double2 st = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)LA) & a.m_mask, a.fb);
+#pragma unroll
+          for (int k1 = 0; k1 < LB; ++k1) {
+            v[k1] = ctw<INV>(v[k1], make_float2((float)w.x, (float)w.y));
+            if (k1 + 1 < LB) w = cmul(w, st);
+          }
+        }
+        if (scale != 1.0f) {
+#pragma unroll
+          for (int k1 = 0; k1 < LB; ++k1) v[k1] = mk(v[k1].x * scale, v[k1].y * scale);
+        }
+        if constexpr (OUTT == 0) {
+          V* o = out + b * a.bs_out + c;
+#pragma unroll
+          for (int k1 = 0; k1 < LB; ++k1) o[(long long)(k2 + LA * k1) * a.es_out] = v[k1];
+        } else {
+          V* o = out + b * a.bs_out + c * a.es_out + k2;
+#pragma unroll
+          for (int k1 = 0; k1 < LB; ++k1) o[LA * k1] = v[k1];
+        }
+      }
+      sy();  // all scratch reads of this item done
+      if (a.discard) {
+        constexpr int LINES = LB * KB * F * 8 / 128;
+        for (int i = tid; i < LINES; i += 256) {
+          const V* q;
+          if constexpr (OUTT == 0) {
+            const int n1 = i / KB, k2 = kb * KB + i % KB;
+            q = scr + ((size_t)n1 * LA + k2) * F;
+          } else {
+            constexpr int LPR = KB * 8 / 128;
+            const int row = i / LPR, part = i % LPR;
+            q = scr + (size_t)row * LA + kb * KB + part * 16;
+          }
+          discard_l2(q);
+        }
+        sy();
+      }
+      if (tid == 0) {
+        signal_release(doneB + slot);
+      }
+    }
   }
 }
 
