@@ -495,12 +495,12 @@ k_comb(const C2<Real>* in, C2<Real>* out, CombArgs a, const C2<Real>* __restrict
 // released as soon as its inputs are in registers, so the next tile's load
 // overlaps the butterflies, the exchange (a separate buffer, in NR rounds
 // when the tile is larger than it) and the stores.
-template <typename Real, int L>
+template <typename Real, int L, int F_ = FOf<Real>::v>
 struct CombTmaCfg {
   using V = C2<Real>;
   static constexpr int RMAX = RmaxOf<Real>::v;
   using Sh = Shape<L, RMAX>;
-  static constexpr int F = FOf<Real>::v;
+  static constexpr int F = F_;
   static constexpr int THREADS = F * Sh::T;
   static constexpr int TILE = L * F;                       // elements
   static constexpr int TILE_BYTES = TILE * (int)sizeof(V);
@@ -548,11 +548,11 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-template <typename Real, int L, bool INV, bool TWID, int MODE>
-__global__ void __launch_bounds__(CombTmaCfg<Real, L>::THREADS, CombTmaCfg<Real, L>::MINB)
+template <typename Real, int L, bool INV, bool TWID, int MODE, int F_ = FOf<Real>::v>
+__global__ void __launch_bounds__(CombTmaCfg<Real, L, F_>::THREADS, CombTmaCfg<Real, L, F_>::MINB)
 k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs a, const C2<Real>* __restrict__ tw,
            const double2* __restrict__ wc, const double2* __restrict__ wf, Real scale) {
-  using Cfg = CombTmaCfg<Real, L>;
+  using Cfg = CombTmaCfg<Real, L, F_>;
   using V = C2<Real>;
   using Sh = typename Cfg::Sh;
   constexpr int F = Cfg::F, S = Cfg::S;
@@ -745,10 +745,11 @@ __device__ __forceinline__ void final_tile(const C2<Real>* in, C2<Real>* out, co
 }
 
 template <typename Real, int L, bool INV, int F_ = FOf<Real>::v>
-__global__ void __launch_bounds__(FinalCfg<Real, L, F_>::THREADS)
+__global__ void __launch_bounds__(FinalCfg<Real, L, F_>::THREADS, FinalCfg<Real, L, F_>::THREADS <= 256 ? 2 : 1)
 k_final_t(const C2<Real>* in, C2<Real>* out, FinalArgs a, const C2<Real>* __restrict__ tw, Real scale) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   final_tile<Real, L, INV, F_>(in, out, a, tw, scale, blockIdx.x, reinterpret_cast<C2<Real>*>(smem_raw));
 }
+
 
 }  // namespace tfb

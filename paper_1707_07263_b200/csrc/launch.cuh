@@ -15,6 +15,11 @@ inline bool env_set(const char* name) {
   return e && *e && *e != '0';
 }
 
+inline int env_int_or(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? std::atoi(e) : dflt;
+}
+
 inline int sm_count() {
   static int n[16] = {0};
   int dev = 0;
@@ -106,9 +111,9 @@ inline bool two_ws_enabled() {
 }
 
 // Strided comb tile as a 4-D tensor {column (8-byte words), n, rr, group}.
-template <typename Real, int L>
+template <typename Real, int L, int F_ = tfb::FOf<Real>::v>
 bool encode_comb_map(CUtensorMap* map, const Pass& ps, const void* in) {
-  using Cfg = tfb::CombTmaCfg<Real, L>;
+  using Cfg = tfb::CombTmaCfg<Real, L, F_>;
   constexpr int W = (int)sizeof(tfb::C2<Real>) / 8;
   auto enc = tensor_map_encoder();
   if (!enc || ((uintptr_t)in % 16) != 0) return false;
@@ -217,6 +222,46 @@ int launch_comb_w(const Pass& ps, const void* in, void* out, const void* tb, con
   return go(tfb::k_comb_w<L, INV, false, 1>);
 }
 
+// Persistent TMA-pipelined comb pass (K_COMB_TMA) with F-comb tiles.
+template <typename Real, int L, bool INV, int F>
+int launch_comb_tma(const Pass& ps, const CUtensorMap& map, void* out, const void* tb, const void* tb64, Real scale,
+                    cudaStream_t st) {
+  using Cfg = tfb::CombTmaCfg<Real, L, F>;
+  using V = tfb::C2<Real>;
+  const tfb::CombArgs& c = ps.comb;
+  constexpr int K = tfb::FOf<Real>::v / F;  // tiles per plan tile (the plan counts FOf-comb tiles)
+  tfb::CombTmaArgs a{};
+  a.ntiles = c.ntiles * K;
+  a.chunks = c.chunks * K;
+  a.groups_per_batch = c.groups_per_batch;
+  a.rps = c.rps;
+  a.sub_len = c.sub_len;
+  a.es = c.es;
+  a.bstride = c.bstride;
+  a.out_w_last = c.out_w_last;
+  a.final_pass = c.final_pass;
+  a.fvalid = F;
+  a.fb = c.fb;
+  a.p = c.p;
+  a.m_mask = c.m_mask;
+  if (const char* e = std::getenv("TILEFFT_DEBUG_COPYONLY")) a.copy_only = std::atoi(e);
+  for (int i = 0; i < 8; ++i) {
+    a.out_w[i] = c.out_w[i];
+    a.sub_w[i] = c.sub_w[i];
+  }
+  auto k = tfb::k_comb_tma<Real, L, INV, true, 0, F>;
+  if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
+  int bps = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, Cfg::THREADS, Cfg::SMEM));
+  const long long grid = std::max<long long>(1, std::min<long long>(a.ntiles, (long long)sm_count() * std::max(bps, 1)));
+  const V* t = (const V*)tb;
+  const double2* t64 = (const double2*)tb64;
+  k<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, st>>>(map, (V*)out, a, t + ps.tw_off, t64 + ps.wc_off, t64 + ps.wf_off,
+                                                     scale);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 template <typename Real, int L, bool INV>
 int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, Real scale,
                 cudaStream_t st) {
@@ -253,42 +298,11 @@ int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, const
     CUtensorMap map;
     // TMA pipelining pays off on the long 1D comb passes (2^30: 13.3 -> 11.8 ms);
     // the short 2D column passes (L <= 128) run faster as many tiny CTAs.
-    if (!ps.no_tma && ps.kind == K_COMB1D && encode_comb_map<Real, L>(&map, ps, in)) {
-      using Cfg = tfb::CombTmaCfg<Real, L>;
-      tfb::CombTmaArgs a{};
-      const tfb::CombArgs& c = ps.comb;
-      a.ntiles = c.ntiles;
-      a.chunks = c.chunks;
-      a.groups_per_batch = c.groups_per_batch;
-      a.rps = c.rps;
-      a.sub_len = c.sub_len;
-      a.es = c.es;
-      a.bstride = c.bstride;
-      a.out_w_last = c.out_w_last;
-      a.final_pass = c.final_pass;
-      a.fvalid = c.fvalid;
-      a.fb = c.fb;
-      a.p = c.p;
-      a.m_mask = c.m_mask;
-      if (const char* e = std::getenv("TILEFFT_DEBUG_COPYONLY")) a.copy_only = std::atoi(e);
-      for (int i = 0; i < 8; ++i) {
-        a.out_w[i] = c.out_w[i];
-        a.sub_w[i] = c.sub_w[i];
-      }
-      auto go = [&](auto k) -> int {
-        if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
-        int bps = 0;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, Cfg::THREADS, Cfg::SMEM));
-        const long long grid = std::max<long long>(1, std::min<long long>(c.ntiles, (long long)sm_count() * std::max(bps, 1)));
-        k<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, st>>>(map, (V*)out, a, t + ps.tw_off, t64 + ps.wc_off,
-                                                           t64 + ps.wf_off, scale);
-        CUDA_TRY(cudaGetLastError());
-        return 0;
-      };
-      if (ps.kind == K_COMB1D) return go(tfb::k_comb_tma<Real, L, INV, true, 0>);
-      if (ps.twid) return go(tfb::k_comb_tma<Real, L, INV, true, 1>);
-      return go(tfb::k_comb_tma<Real, L, INV, false, 1>);
-    }
+    // (8-comb tiles -- 64-byte rows, half the shared memory -- measured 15.8 vs
+    // 11.9 ms at 2^30: the 128-byte line per comb step is what keeps the
+    // strided TMA reads at full DRAM efficiency)
+    if (!ps.no_tma && ps.kind == K_COMB1D && encode_comb_map<Real, L>(&map, ps, in))
+      return launch_comb_tma<Real, L, INV, tfb::FOf<Real>::v>(ps, map, out, tb, tb64, scale, st);
   }
   using Cfg = tfb::CombCfg<Real, L>;
   auto go = [&](auto k) -> int {
@@ -302,7 +316,6 @@ int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, const
   if (ps.twid) return go(tfb::k_comb<Real, L, INV, true, 1>);
   return go(tfb::k_comb<Real, L, INV, false, 1>);
 }
-
 template <typename Real, int L, bool INV>
 int launch_final(const Pass& ps, const void* in, void* out, const void* tb, const void*, Real scale,
                  cudaStream_t st) {
@@ -322,6 +335,9 @@ int launch_final(const Pass& ps, const void* in, void* out, const void* tb, cons
       return 0;
     }
   }
+  // (a persistent TMA-prefetching variant -- 16 bulk row copies per tile, exchange
+  // and transpose in two rounds to make room for the slot -- measured slower at
+  // 2^30: 12.41 vs 11.82 ms)
   using Cfg = tfb::FinalCfg<Real, L>;
   auto k = tfb::k_final_t<Real, L, INV>;
   if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
