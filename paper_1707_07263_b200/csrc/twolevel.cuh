@@ -444,9 +444,14 @@ k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, Two
         fence_proxy_async_smem();
         sy();  // slot s consumed (and s_a_* of slot s read by every thread)
         if (tid == 0) grab_into(s);
-        V* reg = xb + fx * Cfg::REG;
-        auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
-        Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
+        if constexpr (OUTT == 0) {
+          auto ex = [xb, fx](int i) -> V& { return xb[i * Cfg::FX + fx]; };
+          Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
+        } else {
+          V* reg = xb + fx * Cfg::REG;
+          auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
+          Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
+        }
       }
       (void)fx;
       (void)my_round;

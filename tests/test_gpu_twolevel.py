@@ -98,9 +98,12 @@ def test_two_level_inverse_vs_oracle(tf, oracle):
     assert rel_l2(got, oracle.fft_tiled(x, inverse=True)) <= tol(n)
 
 
-def test_two_level_schedule_invariance(tf, oracle, monkeypatch):
+@pytest.mark.parametrize("ws", ["1", "0"])
+def test_two_level_schedule_invariance(tf, oracle, monkeypatch, ws):
     """Lag D and slot count only change which CTA runs which item and when:
-    the output is bit-identical (D=1 with 2 slots makes every dependency wait)."""
+    the output is bit-identical (D=1 with 2 slots makes every dependency wait).
+    ws=1: the warp-specialised kernel (default), ws=0: the mixed-item kernel."""
+    monkeypatch.setenv("TILEFFT_TWO_WS", ws)
     n = 1 << 24
     x = oracle.random_bench_signal(n, 3).astype(np.complex64)
     ref = _run(_plan(tf, n), x)
@@ -194,3 +197,44 @@ def test_warp_owned_comb_kernel_2d_opt_in(tf, oracle, monkeypatch, ny, nx):
     out = np.empty_like(img)
     dp.exec_host(img.ctypes.data, out.ctypes.data, tf._capi.FORWARD)
     assert rel_l2(out, oracle.fft2(img)) <= tol(ny * nx)
+
+
+@pytest.mark.parametrize("case", ["1d", "2d"])
+def test_two_level_warp_specialised_matches_mixed_kernel(tf, oracle, monkeypatch, case):
+    """k_two_ws (A team / B team, W_L^{n1 k2} applied by the B team) vs k_two
+    (one item queue, root applied by the A item): same transform."""
+    def run():
+        if case == "1d":
+            n = 1 << 23
+            x = oracle.random_bench_signal(n, 8).astype(np.complex64)
+            return _run(_plan(tf, n), x), oracle.fft_tiled(x), n
+        img = oracle.random_bench_signal(4096 * 512, 8).astype(np.complex64).reshape(4096, 512)
+        dp = tf._capi.DevicePlan.create_2d(4096, 512, 1, 8, 0)
+        out = np.empty_like(img)
+        dp.exec_host(img.ctypes.data, out.ctypes.data, tf._capi.FORWARD)
+        return out, oracle.fft2(img), img.size
+    a, want, n = run()
+    monkeypatch.setenv("TILEFFT_TWO_WS", "0")
+    b, _, _ = run()
+    assert rel_l2(a, want) <= tol(n) and rel_l2(b, want) <= tol(n)
+    assert rel_l2(a, b) < 1e-6
+
+
+@pytest.mark.parametrize("logn", [14, 15, 18, 19, 20])
+def test_fused_small_two_pass_opt_in(tf, oracle, monkeypatch, logn):
+    """K_SMALL2 (TILEFFT_FUSE=1): both passes of a small plan in one launch with
+    a dynamic tile counter; repeated executions exercise the monotonic counters."""
+    monkeypatch.setenv("TILEFFT_FUSE", "1")
+    monkeypatch.delenv("TILEFFT_TWO_1D", raising=False)
+    n = 1 << logn
+    dp = _plan(tf, n)
+    info = dp.info()
+    assert info["launches_per_exec"] == 1 and info["passes"] == 2
+    x = oracle.random_bench_signal(n, 9).astype(np.complex64)
+    want = oracle.fft_tiled(x)
+    first = _run(dp, x)
+    assert rel_l2(first, want) <= tol(n) and rel_l2(first, want) < 5e-7
+    for _ in range(3):
+        assert bits_equal(_run(dp, x), first)
+    inv = _run(dp, x, tf._capi.INVERSE)
+    assert rel_l2(inv, oracle.fft_tiled(x, inverse=True)) <= tol(n)
