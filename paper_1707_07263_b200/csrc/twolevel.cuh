@@ -355,6 +355,11 @@ k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, Two
          const float2* __restrict__ twl, const double2* __restrict__ wc, const double2* __restrict__ wf, float scale) {
   using Cfg = typename TwoWsCfg<LA, LB, INV, OUTT>::Base;
   constexpr int NS = TwoWsCfg<LA, LB, INV, OUTT>::NS;
+  // Who applies W_L^{n1 k2}: the B team when it has spare time (no inter-pass
+  // root: 8192^2 column pass 396 -> 341 us), the A team when the B team also
+  // carries the inter-pass root W_M^{c k} (TWID) and would fall behind (a
+  // lagging B team lets the scratch ring outgrow L2 and spill to DRAM).
+  constexpr bool TWL_IN_B = !TWID;
   using V = float2;
   using Sh = typename Cfg::Sh;
   constexpr int F = Cfg::F, T = Cfg::T, KB = Cfg::KB;
@@ -455,6 +460,13 @@ k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, Two
       }
       (void)fx;
       (void)my_round;
+      if constexpr (!TWL_IN_B) {
+#pragma unroll
+        for (int j = 0; j < Sh::R; ++j) {
+          const int k2 = out_index<LA, 32>(t, j);
+          v[j] = ctw<INV>(v[j], __ldg(twl + n1 * k2));
+        }
+      }
       if (tid == 0 && gen > 0) wait_geq(doneB + slot, gen * LB);
       sy();
       if constexpr (OUTT == 0) {
@@ -464,10 +476,9 @@ k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, Two
 #pragma unroll
         for (int j = 0; j < Sh::R; ++j) scr[((size_t)n1 * F + f) * LA + out_index<LA, 32>(t, j)] = v[j];
       }
+      // (a per-warp release without this barrier measured slower: 356 vs 341 us)
       sy();
-      if (tid == 0) {
-        signal_release(doneA + slot);
-      }
+      if (tid == 0) signal_release(doneA + slot);
     }
   } else {
     // ============================================================ B team
@@ -508,18 +519,37 @@ k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, Two
           const V* q = OUTT == 0 ? scr + ((size_t)n1 * LA + k2) * F + f : scr + ((size_t)n1 * F + f) * LA + k2;
           v[n1] = __ldcg(q);
         }
-        // W_L^{n1 k2}, deferred from the A item: the A team is the critical path
+        // W_L^{n1 k2}, deferred from the A item when the A team is the critical path
+        if constexpr (TWL_IN_B) {
 #pragma unroll
-        for (int n1 = 1; n1 < LB; ++n1) v[n1] = ctw<INV>(v[n1], __ldg(twl + n1 * k2));
+          for (int n1 = 1; n1 < LB; ++n1) v[n1] = ctw<INV>(v[n1], __ldg(twl + n1 * k2));
+        }
         reg_dft<LB, INV>(v);
         const long long c = ch * F + f;
         if constexpr (TWID) {
-          double2 w = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)k2) & a.m_mask, a.fb);
-          const double2 st = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)LA) & a.m_mask, a.fb);
+          // W_M^{c (k2 + LA k1)} = B[k1 % 4] * A[k1 / 4] with B[b] = W^{c k2} s^b,
+          // A[a] = s^{4a}, s = W^{c LA}: built in fp64 (depth ~4 instead of a
+          // 15-long dependent chain), each rounded once, product in fp32
+          constexpr int QA = LB / 4 > 0 ? LB / 4 : 1;
+          const double2 w0 = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)k2) & a.m_mask, a.fb);
+          const double2 s1 = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)LA) & a.m_mask, a.fb);
+          const double2 s2 = cmul(s1, s1), s4 = cmul(s2, s2);
+          const double2 w2 = cmul(w0, s2);
+          const V Bq[4] = {to_v(w0, (V*)nullptr), to_v(cmul(w0, s1), (V*)nullptr), to_v(w2, (V*)nullptr),
+                           to_v(cmul(w2, s1), (V*)nullptr)};
+          V Aq[QA];
+          {
+            double2 p = make_double2(1.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < QA; ++q) {
+              Aq[q] = to_v(p, (V*)nullptr);
+              if (q + 1 < QA) p = cmul(p, s4);
+            }
+          }
 #pragma unroll
           for (int k1 = 0; k1 < LB; ++k1) {
-            v[k1] = ctw<INV>(v[k1], make_float2((float)w.x, (float)w.y));
-            if (k1 + 1 < LB) w = cmul(w, st);
+            const V w = k1 < 4 ? Bq[k1 % 4] : cmul(Aq[k1 / 4], Bq[k1 % 4]);
+            v[k1] = ctw<INV>(v[k1], w);
           }
         }
         if (scale != 1.0f) {
