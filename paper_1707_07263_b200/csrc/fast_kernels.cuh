@@ -85,15 +85,22 @@ __device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
 // ------------------------------------------------------------------ Stockham
 // v[i*RS + q]: input q of butterfly b = t + T*i of the current stage.
 // After the last stage v[i*RS + q] = X[b + q * (L / RS_last)].
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
 template <typename V, int L, int RMAX, bool INV, int S, int NR = 1>
 struct Stages {
   using Sh = Shape<L, RMAX>;
   static constexpr int RS = Sh::radix(S), NS = Sh::ns(S), NB = Sh::R / RS;
   // NR > 1: the exchange buffer holds 1/NR of the CTA's FFTs; the exchange
   // runs in NR rounds and a thread takes part in round `my_round` only.
-  template <class Ex, class Sync>
+  // `last` runs at the start of the last stage, once the exchange buffer is
+  // free (multi-stage networks only): e.g. to start streaming the next input.
+  template <class Ex, class Sync, class Hook = NoHook>
   __device__ __forceinline__ static void run(V* v, int t, Ex& ex, const V* __restrict__ tw, Sync& sync,
-                                             int my_round = 0) {
+                                             int my_round = 0, Hook last = Hook{}) {
+    if constexpr (S > 0 && S + 1 == Sh::NST) last();
     if constexpr (S > 0) {
       const V* tws = tw + Sh::tw_off(S);
 #pragma unroll
@@ -129,7 +136,7 @@ struct Stages {
         }
         sync();
       }
-      Stages<V, L, RMAX, INV, S + 1, NR>::run(v, t, ex, tw, sync, my_round);
+      Stages<V, L, RMAX, INV, S + 1, NR>::run(v, t, ex, tw, sync, my_round, last);
     }
   }
 };
@@ -751,5 +758,70 @@ k_final_t(const C2<Real>* in, C2<Real>* out, FinalArgs a, const C2<Real>* __rest
   final_tile<Real, L, INV, F_>(in, out, a, tw, scale, blockIdx.x, reinterpret_cast<C2<Real>*>(smem_raw));
 }
 
+
+// ------------------------------------------------------------------ K_ROWS_PF
+// Persistent K_ROWS for long fp32 rows (L = 2048..8192: one CTA per row,
+// 2 CTAs per SM). The row's shared-memory exchange region doubles as the
+// landing zone of the NEXT row: as soon as the last exchange is done, one
+// bulk copy (TMA, 1D) streams the next row in, so its DRAM latency overlaps
+// the last radix stage and the stores of the current row. The first read of
+// a row (lanes along n, unpadded) is bank-conflict free without the pad.
+template <int L>
+struct RowsPfCfg {
+  using Sh = Shape<L, 32>;
+  static constexpr int THREADS = Sh::T;
+  static constexpr int REG = L + L / 32 + 1;
+  static constexpr int SMEM = REG * 8 + 16;
+};
+
+template <int L, bool INV>
+__global__ void __launch_bounds__(RowsPfCfg<L>::THREADS, 2)
+k_rows_pf(const float2* __restrict__ in, float2* __restrict__ out, long long nrows, const float2* __restrict__ tw,
+          float scale) {
+  using Cfg = RowsPfCfg<L>;
+  using V = float2;
+  using Sh = typename Cfg::Sh;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  V* sm = reinterpret_cast<V*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + Cfg::REG);
+  const int t = threadIdx.x;
+  long long row = blockIdx.x;
+  auto issue = [&](long long r) {
+    mbar_arrive_expect_tx(full, L * 8);
+    tma_load_1d(sm, in + r * L, L * 8, full);
+  };
+  if (t == 0) {
+    mbar_init(full, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (t == 0 && row < nrows) issue(row);
+  uint32_t phase = 0;
+#pragma unroll 1
+  for (; row < nrows; row += gridDim.x) {
+    mbar_wait(full, phase);
+    phase ^= 1;
+    V v[Sh::R];
+#pragma unroll
+    for (int q = 0; q < Sh::R; ++q) v[q] = sm[t + q * Sh::T];
+    __syncthreads();  // the exchange below overwrites the landing zone
+    auto ex = [sm](int i) -> V& { return sm[pad32(i)]; };
+    const long long nxt = row + gridDim.x;
+    auto prefetch = [&]() {
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (t == 0 && nxt < nrows) issue(nxt);
+    };
+    SyncBlock sy;
+    Stages<V, L, 32, INV, 0>::run(v, t, ex, tw, sy, 0, prefetch);
+    V* dst = out + row * L;
+#pragma unroll
+    for (int j = 0; j < Sh::R; ++j) {
+      V r = v[j];
+      if (scale != 1.0f) r = mk(r.x * scale, r.y * scale);
+      dst[out_index<L, 32>(t, j)] = r;
+    }
+  }
+}
 
 }  // namespace tfb

@@ -71,6 +71,20 @@ int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, const
       return 0;
     }
   }
+  if constexpr (std::is_same<Real, float>::value && L >= 2048) {
+    if (aligned && !ps.no_tma && !env_set("TILEFFT_NO_ROWS_PF")) {
+      using CfgP = tfb::RowsPfCfg<L>;
+      auto k = tfb::k_rows_pf<L, INV>;
+      if (int rc = ensure_smem((const void*)k, CfgP::SMEM)) return rc;
+      int bps = 0;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, CfgP::THREADS, CfgP::SMEM));
+      const long long grid = std::max<long long>(1, std::min<long long>(ps.nrows, (long long)sm_count() * std::max(bps, 1)));
+      k<<<(unsigned)grid, CfgP::THREADS, CfgP::SMEM, st>>>((const float2*)in, (float2*)out, ps.nrows,
+                                                           (const float2*)tw + ps.tw_off, (float)scale);
+      CUDA_TRY(cudaGetLastError());
+      return 0;
+    }
+  }
   constexpr int FPC = rows_fpc<Real>(L);
   using Cfg = tfb::RowsCfg<Real, L, FPC>;
   auto k = tfb::k_rows<Real, L, FPC, INV>;
