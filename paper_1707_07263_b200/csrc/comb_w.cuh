@@ -68,6 +68,7 @@ template <int L, bool INV, bool TWID, int MODE>
 __global__ void __launch_bounds__(CombWCfg<L>::THREADS, 1)
 k_comb_w(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, CombTmaArgs a,
          const float2* __restrict__ tw, const double2* __restrict__ wc, const double2* __restrict__ wf, float scale) {
+  pdl_enter();
   using Cfg = CombWCfg<L>;
   using V = float2;
   using Sh = Shape<L, 32>;

@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(Small2Cfg<L1, L2>::THREADS)
 k_small2(const float2* in, float2* work, float2* out, CombArgs a1, FinalArgs a2, const float2* __restrict__ tw1,
          const float2* __restrict__ tw2, const double2* __restrict__ wc, const double2* __restrict__ wf, float scale,
          unsigned long long* ctr) {
+  pdl_enter();
   using Cfg = Small2Cfg<L1, L2>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* sm = reinterpret_cast<float2*>(smem_raw);

@@ -835,6 +835,42 @@ int tilefft_plan_create_2d(tilefft_plan_t* out, uint64_t ny, uint64_t nx, uint64
   return 0;
 }
 
+namespace {
+// Programmatic dependent launch inside a captured plan: every kernel -> kernel
+// edge becomes a programmatic edge, so pass s+1 is launched while pass s
+// drains and waits (griddepcontrol.wait, pdl_enter in every fast kernel) for
+// its completion before reading. Only FAST plans, whose kernels all call
+// pdl_enter; memset nodes keep ordinary edges. Any failure leaves the graph
+// as captured (the replay is then just not overlapped).
+void make_programmatic(cudaGraph_t graph) {
+  size_t ne = 0;
+  if (cudaGraphGetEdges(graph, nullptr, nullptr, &ne) != cudaSuccess || ne == 0) {
+    cudaGetLastError();
+    return;
+  }
+  std::vector<cudaGraphNode_t> from(ne), to(ne);
+  if (cudaGraphGetEdges(graph, from.data(), to.data(), &ne) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  for (size_t i = 0; i < ne; ++i) {
+    cudaGraphNodeType a, b;
+    if (cudaGraphNodeGetType(from[i], &a) != cudaSuccess || cudaGraphNodeGetType(to[i], &b) != cudaSuccess) break;
+    if (a != cudaGraphNodeTypeKernel || b != cudaGraphNodeTypeKernel) continue;
+    if (cudaGraphRemoveDependencies(graph, &from[i], &to[i], 1) != cudaSuccess) break;
+    cudaGraphEdgeData ed{};
+    ed.from_port = cudaGraphKernelNodePortProgrammatic;
+    ed.type = cudaGraphDependencyTypeProgrammatic;
+    if (cudaGraphAddDependencies_v2(graph, &from[i], &to[i], &ed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      cudaGraphAddDependencies(graph, &from[i], &to[i], 1);  // restore the plain edge
+      break;
+    }
+  }
+  cudaGetLastError();
+}
+}  // namespace
+
 int tilefft_exec_c2c(tilefft_plan_t P, const void* in, void* out, int sign, void* stream) {
   g_err.clear();
   if (!P) return fail(TILEFFT_EINVAL, "tilefft_exec_c2c: null plan");
@@ -866,6 +902,10 @@ int tilefft_exec_c2c(tilefft_plan_t P, const void* in, void* out, int sign, void
     return rc;
   }
   if (ce != cudaSuccess) return fail(TILEFFT_ECUDA, "stream capture failed: %s", cudaGetErrorString(ce));
+  // opt-in (TILEFFT_PDL=1): measured neutral with the implicit trigger at CTA exit
+  // (2^14..2^30, 8192^2 within noise) and mixed with an early trigger (2^16
+  // 10.2 -> 8.2 us, 2^20 14.3 -> 16.4 us, 2^30 11.84 -> 12.07 ms)
+  if (P->mode == TILEFFT_MODE_FAST && env_flag("TILEFFT_PDL")) make_programmatic(graph);
   cudaGraphExec_t exec = nullptr;
   const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);

@@ -124,6 +124,7 @@ template <int LA, int LB, bool INV, int OUTT, bool TWID>
 __global__ void __launch_bounds__(256, 2)
 k_two(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, TwoArgs a, const float2* __restrict__ tw,
       const float2* __restrict__ twl, const double2* __restrict__ wc, const double2* __restrict__ wf, float scale) {
+  pdl_enter();
   using Cfg = TwoCfg<LA, LB, INV, OUTT>;
   using V = float2;
   using Sh = typename Cfg::Sh;
@@ -353,6 +354,7 @@ template <int LA, int LB, bool INV, int OUTT, bool TWID>
 __global__ void __launch_bounds__(512, 1)
 k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, TwoArgs a, const float2* __restrict__ tw,
          const float2* __restrict__ twl, const double2* __restrict__ wc, const double2* __restrict__ wf, float scale) {
+  pdl_enter();
   using Cfg = typename TwoWsCfg<LA, LB, INV, OUTT>::Base;
   constexpr int NS = TwoWsCfg<LA, LB, INV, OUTT>::NS;
   // Who applies W_L^{n1 k2}: the B team when it has spare time (no inter-pass

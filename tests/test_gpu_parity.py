@@ -195,3 +195,19 @@ def test_stage_row_fft_and_interstage(tf, oracle):
     b.cells[0, :2] = [1.0, 1.0]
     tf.apply_interstage_twiddles(b, 1, plan, tf.build_twiddle_table(16))
     assert b.tile()[0, 0] == 1.0 and b.tile()[0, 1] == -1j
+
+
+@pytest.mark.parametrize("n", [1 << 16, 1 << 20, 1 << 24])
+def test_fast_mode_programmatic_launch_opt_in(tf, oracle, monkeypatch, n):
+    """TILEFFT_PDL=1: the plan's graph has programmatic kernel->kernel edges and
+    every pass waits (griddepcontrol.wait) for its predecessor: same output."""
+    x = oracle.random_bench_signal(n, 4).astype(np.complex64)
+    dp = tf._capi.DevicePlan.create(n, 1, None, 8, tf._capi.MODE_FAST, None, 0)
+    ref = np.empty_like(x)
+    dp.exec_host(x.ctypes.data, ref.ctypes.data, tf._capi.FORWARD)
+    monkeypatch.setenv("TILEFFT_PDL", "1")
+    dq = tf._capi.DevicePlan.create(n, 1, None, 8, tf._capi.MODE_FAST, None, 0)
+    for _ in range(3):
+        got = np.empty_like(x)
+        dq.exec_host(x.ctypes.data, got.ctypes.data, tf._capi.FORWARD)
+        assert bits_equal(got, ref)
