@@ -75,7 +75,9 @@ def measured_peaks():
 
 
 def profile_traffic(config: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    """DRAM bytes (ncu dram__bytes_read + dram__bytes_write) per step from the committed launch lists
+    (profiles/r01_launches_*_s3.csv): the one launch for single-pass plans, the sum over one step's
+    passes for multi-pass plans (matching `achieved`, which is per step)."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
