@@ -89,7 +89,9 @@ struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
 
-template <typename V, int L, int RMAX, bool INV, int S, int NR = 1>
+// TWS: the stage-root table `tw` lives in shared memory (plain loads -> LDS)
+// instead of global memory read through the read-only path (LDG.CONSTANT).
+template <typename V, int L, int RMAX, bool INV, int S, int NR = 1, bool TWS = false>
 struct Stages {
   using Sh = Shape<L, RMAX>;
   static constexpr int RS = Sh::radix(S), NS = Sh::ns(S), NB = Sh::R / RS;
@@ -107,7 +109,12 @@ struct Stages {
       for (int i = 0; i < NB; ++i) {
         const int k = (t + Sh::T * i) & (NS - 1);
 #pragma unroll
-        for (int q = 1; q < RS; ++q) v[i * RS + q] = ctw<INV>(v[i * RS + q], __ldg(tws + q * NS + k));
+        for (int q = 1; q < RS; ++q) {
+          V w;
+          if constexpr (TWS) w = tws[q * NS + k];
+          else w = __ldg(tws + q * NS + k);
+          v[i * RS + q] = ctw<INV>(v[i * RS + q], w);
+        }
       }
     }
 #pragma unroll
@@ -136,7 +143,7 @@ struct Stages {
         }
         sync();
       }
-      Stages<V, L, RMAX, INV, S + 1, NR>::run(v, t, ex, tw, sync, my_round, last);
+      Stages<V, L, RMAX, INV, S + 1, NR, TWS>::run(v, t, ex, tw, sync, my_round, last);
     }
   }
 };
@@ -291,17 +298,26 @@ struct RowsTmaCfg {
   static constexpr int THREADS = WARPS * 32;
   static constexpr int DATA_BYTES = WARPS * S * SLOT * (int)sizeof(V);
   static constexpr int SMEM = DATA_BYTES + WARPS * S * 8;
+  static constexpr int TW_BYTES = Sh::TW_TOTAL * (int)sizeof(V);  // stage roots staged in smem (TWS variant)
 };
 
-template <typename Real, int L, int WARPS, int S, bool INV>
+template <typename Real, int L, int WARPS, int S, bool INV, bool TWS = false>
 __global__ void __launch_bounds__(WARPS * 32)
-k_rows_tma(const C2<Real>* in, C2<Real>* out, long long nrows, const C2<Real>* __restrict__ tw, Real scale) {
+k_rows_tma(const C2<Real>* in, C2<Real>* out, long long nrows, const C2<Real>* __restrict__ tw_g, Real scale) {
   pdl_enter();
   using Cfg = RowsTmaCfg<Real, L, WARPS, S>;
   using V = C2<Real>;
   using Sh = typename Cfg::Sh;
   constexpr int FPW = Cfg::FPW;
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  const V* tw = tw_g;
+  if constexpr (TWS) {
+    // stage the plan's stage-root table once per CTA (persistent kernel)
+    V* tws = reinterpret_cast<V*>(smem_raw + Cfg::SMEM);
+    for (int i = threadIdx.x; i < Sh::TW_TOTAL; i += blockDim.x) tws[i] = tw_g[i];
+    __syncthreads();
+    tw = tws;
+  }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ff = lane / Sh::T, tt = lane % Sh::T;
   V* slots = reinterpret_cast<V*>(smem_raw) + (size_t)w * S * Cfg::SLOT;
@@ -347,11 +363,11 @@ k_rows_tma(const C2<Real>* in, C2<Real>* out, long long nrows, const C2<Real>* _
       __syncwarp();
       auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
       SyncWarp sy;
-      Stages<V, L, Cfg::RMAX, INV, 0>::run(v, tt, ex, tw, sy);
+      Stages<V, L, Cfg::RMAX, INV, 0, 1, TWS>::run(v, tt, ex, tw, sy);
     } else {
       auto ex = [reg](int i) -> V& { return reg[i]; };
       SyncWarp sy;
-      Stages<V, L, Cfg::RMAX, INV, 0>::run(v, tt, ex, tw, sy);
+      Stages<V, L, Cfg::RMAX, INV, 0, 1, TWS>::run(v, tt, ex, tw, sy);
     }
     const long long row = c * FPW + ff;
     if (row < nrows) {

@@ -50,14 +50,18 @@ int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, const
   if constexpr (T <= 32) {
     if (aligned && !ps.no_tma) {
       using Cfg = tfb::RowsTmaCfg<Real, L, kRowsWarps, kRowsStages>;
-      auto k = tfb::k_rows_tma<Real, L, kRowsWarps, kRowsStages, INV>;
-      if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
-      static int blocks_per_sm[16] = {0};
+      // TILEFFT_TW_SMEM=1: stage roots from shared memory instead of the read-only path (measurement switch)
+      const bool tws = tfb::Shape<L, tfb::RmaxOf<Real>::v>::NST > 1 && env_int_or("TILEFFT_TW_SMEM", 0);
+      auto k = tws ? tfb::k_rows_tma<Real, L, kRowsWarps, kRowsStages, INV, true>
+                   : tfb::k_rows_tma<Real, L, kRowsWarps, kRowsStages, INV, false>;
+      const int smem = Cfg::SMEM + (tws ? Cfg::TW_BYTES : 0);
+      if (int rc = ensure_smem((const void*)k, smem)) return rc;
+      static int blocks_per_sm[2][16] = {};
       int dev = 0;
       cudaGetDevice(&dev);
-      int& bps = blocks_per_sm[dev & 15];
+      int& bps = blocks_per_sm[tws ? 1 : 0][dev & 15];
       if (!bps) {
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, Cfg::THREADS, Cfg::SMEM));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, Cfg::THREADS, smem));
         if (bps < 1) bps = 1;
       }
       int sms = 0;
@@ -65,8 +69,8 @@ int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, const
       const long long chunks = (ps.nrows + Cfg::FPW - 1) / Cfg::FPW;
       const long long want = (chunks + kRowsWarps - 1) / kRowsWarps;
       const long long grid = std::max<long long>(1, std::min<long long>(want, (long long)sms * bps));
-      k<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, st>>>((const tfb::C2<Real>*)in, (tfb::C2<Real>*)out, ps.nrows,
-                                                         (const tfb::C2<Real>*)tw + ps.tw_off, scale);
+      k<<<(unsigned)grid, Cfg::THREADS, smem, st>>>((const tfb::C2<Real>*)in, (tfb::C2<Real>*)out, ps.nrows,
+                                                    (const tfb::C2<Real>*)tw + ps.tw_off, scale);
       CUDA_TRY(cudaGetLastError());
       return 0;
     }
