@@ -343,11 +343,9 @@ struct TwoWsCfg {
   // L1 for the twiddle tables and measured slower (618 vs 585 us, 8192^2)
   using Base = TwoCfg<LA, LB, INV, OUTT, 2>;
   static constexpr int NS = 2;  // A tile slots
-  // INPLACE: exchange in the consumed tile slot (one round, refill after the
-  // FFT) instead of a separate half-tile buffer -- measured slower at 8192^2
-  // (615 vs 550 us with 2 or 3 slots), so off.
-  static constexpr bool INPLACE = false;
-  static constexpr int SMEM = NS * Base::TILE_BYTES + (INPLACE ? 0 : Base::XB * 8) + NS * 8 + 1024;
+  // (exchanging in place in the consumed tile slot -- one round, slot refilled
+  // after the FFT -- measured slower at 8192^2: 615 vs 550 us with 2 or 3 slots)
+  static constexpr int SMEM = NS * Base::TILE_BYTES + Base::XB * 8 + NS * 8 + 1024;
 };
 
 template <int LA, int LB, bool INV, int OUTT, bool TWID>
@@ -371,7 +369,7 @@ k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, Two
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   V* tiles = reinterpret_cast<V*>(base);
   V* xb = tiles + NS * Cfg::TILE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(xb + (TwoWsCfg<LA, LB, INV, OUTT>::INPLACE ? 0 : Cfg::XB));
+  uint64_t* full = reinterpret_cast<uint64_t*>(xb + Cfg::XB);
   __shared__ long long s_a_g[NS];
   __shared__ int s_a_sub[NS];
   __shared__ long long s_b_id;
@@ -439,29 +437,17 @@ k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, Two
         }
       }
       const int my_round = f / Cfg::FX, fx = f % Cfg::FX;
-      if constexpr (TwoWsCfg<LA, LB, INV, OUTT>::INPLACE) {
-        sy();  // every thread has its inputs (and s_a_* of slot s) before the exchange overwrites the slot
-        V* tw_slot = tiles + s * Cfg::TILE;
-        auto ex = [tw_slot, f](int i) -> V& { return tw_slot[i * F + f]; };
-        Stages<V, LA, 32, INV, 0, 1>::run(v, t, ex, tw, sy, 0);
-        fence_proxy_async_smem();
-        sy();  // exchange done: refill the slot
-        if (tid == 0) grab_into(s);
+      fence_proxy_async_smem();
+      sy();  // slot s consumed (and s_a_* of slot s read by every thread)
+      if (tid == 0) grab_into(s);
+      if constexpr (OUTT == 0) {
+        auto ex = [xb, fx](int i) -> V& { return xb[i * Cfg::FX + fx]; };
+        Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
       } else {
-        fence_proxy_async_smem();
-        sy();  // slot s consumed (and s_a_* of slot s read by every thread)
-        if (tid == 0) grab_into(s);
-        if constexpr (OUTT == 0) {
-          auto ex = [xb, fx](int i) -> V& { return xb[i * Cfg::FX + fx]; };
-          Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
-        } else {
-          V* reg = xb + fx * Cfg::REG;
-          auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
-          Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
-        }
+        V* reg = xb + fx * Cfg::REG;
+        auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
+        Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
       }
-      (void)fx;
-      (void)my_round;
       if constexpr (!TWL_IN_B) {
 #pragma unroll
         for (int j = 0; j < Sh::R; ++j) {
