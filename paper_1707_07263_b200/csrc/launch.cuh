@@ -42,6 +42,30 @@ constexpr int rows_fpc(int L) {
 constexpr int kRowsWarps = 4;
 constexpr int kRowsStages = 2;
 
+// one persistent TMA rows launch with W warps per CTA and an S-deep ring per warp
+template <typename Real, int L, bool INV, int W, int S, bool TWS>
+int launch_rows_tma(const Pass& ps, const void* in, void* out, const void* tw, Real scale, cudaStream_t st) {
+  using Cfg = tfb::RowsTmaCfg<Real, L, W, S>;
+  auto k = tfb::k_rows_tma<Real, L, W, S, INV, TWS>;
+  const int smem = Cfg::SMEM + (TWS ? Cfg::TW_BYTES : 0);
+  if (int rc = ensure_smem((const void*)k, smem)) return rc;
+  static int blocks_per_sm[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& bps = blocks_per_sm[dev & 15];
+  if (!bps) {
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, Cfg::THREADS, smem));
+    if (bps < 1) bps = 1;
+  }
+  const long long chunks = (ps.nrows + Cfg::FPW - 1) / Cfg::FPW;
+  const long long want = (chunks + W - 1) / W;
+  const long long grid = std::max<long long>(1, std::min<long long>(want, (long long)sm_count() * bps));
+  k<<<(unsigned)grid, Cfg::THREADS, smem, st>>>((const tfb::C2<Real>*)in, (tfb::C2<Real>*)out, ps.nrows,
+                                                (const tfb::C2<Real>*)tw + ps.tw_off, scale);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 template <typename Real, int L, bool INV>
 int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, const void*, Real scale, cudaStream_t st) {
   constexpr int RM = tfb::RmaxOf<Real>::v;
@@ -49,30 +73,12 @@ int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, const
   const bool aligned = ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0) && (L * sizeof(tfb::C2<Real>)) % 16 == 0;
   if constexpr (T <= 32) {
     if (aligned && !ps.no_tma) {
-      using Cfg = tfb::RowsTmaCfg<Real, L, kRowsWarps, kRowsStages>;
       // TILEFFT_TW_SMEM=1: stage roots from shared memory instead of the read-only path (measurement switch)
-      const bool tws = tfb::Shape<L, tfb::RmaxOf<Real>::v>::NST > 1 && env_int_or("TILEFFT_TW_SMEM", 0);
-      auto k = tws ? tfb::k_rows_tma<Real, L, kRowsWarps, kRowsStages, INV, true>
-                   : tfb::k_rows_tma<Real, L, kRowsWarps, kRowsStages, INV, false>;
-      const int smem = Cfg::SMEM + (tws ? Cfg::TW_BYTES : 0);
-      if (int rc = ensure_smem((const void*)k, smem)) return rc;
-      static int blocks_per_sm[2][16] = {};
-      int dev = 0;
-      cudaGetDevice(&dev);
-      int& bps = blocks_per_sm[tws ? 1 : 0][dev & 15];
-      if (!bps) {
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, Cfg::THREADS, smem));
-        if (bps < 1) bps = 1;
-      }
-      int sms = 0;
-      CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      const long long chunks = (ps.nrows + Cfg::FPW - 1) / Cfg::FPW;
-      const long long want = (chunks + kRowsWarps - 1) / kRowsWarps;
-      const long long grid = std::max<long long>(1, std::min<long long>(want, (long long)sms * bps));
-      k<<<(unsigned)grid, Cfg::THREADS, smem, st>>>((const tfb::C2<Real>*)in, (tfb::C2<Real>*)out, ps.nrows,
-                                                    (const tfb::C2<Real>*)tw + ps.tw_off, scale);
-      CUDA_TRY(cudaGetLastError());
-      return 0;
+      if (tfb::Shape<L, RM>::NST > 1 && env_int_or("TILEFFT_TW_SMEM", 0))
+        return launch_rows_tma<Real, L, INV, kRowsWarps, kRowsStages, true>(ps, in, out, tw, scale, st);
+      // (4 warps x 2-deep rings measured best on batched 1024 x 65536: 0.174 ms; 4x3 0.199, 2x3 0.201,
+      // 2x4 0.196, 8x2 0.195, 1x4 0.187, 1x6 0.242 -- profiles/r01_s3_rows_tma_sweep.txt)
+      return launch_rows_tma<Real, L, INV, kRowsWarps, kRowsStages, false>(ps, in, out, tw, scale, st);
     }
   }
   if constexpr (std::is_same<Real, float>::value && L >= 2048) {
