@@ -211,3 +211,24 @@ def test_fast_mode_programmatic_launch_opt_in(tf, oracle, monkeypatch, n):
         got = np.empty_like(x)
         dq.exec_host(x.ctypes.data, got.ctypes.data, tf._capi.FORWARD)
         assert bits_equal(got, ref)
+
+
+@pytest.mark.parametrize("n,b", [(2048, 300), (4096, 129), (8192, 64)])
+def test_fast_batched_long_rows_prefetch_kernel(tf, oracle, monkeypatch, n, b):
+    """k_rows_pf (persistent long rows, next row streamed into the exchange region):
+    batched through the chunked host pipeline (in place per chunk) and on device
+    buffers, every row against the oracle, and bitwise equal to k_rows."""
+    import torch
+    x = oracle.random_bench_signal(n * b, 6).astype(np.complex64).reshape(b, n)
+    want = oracle.fft_tiled(x)
+    got = tf.fft_tiled(x, tf.make_plan(n))
+    per_row = np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)
+    assert per_row.max() < 1e-6
+    xd = torch.from_numpy(x).cuda()
+    dev = tf.fft_tiled_device(xd, tf.make_plan(n)).cpu().numpy()
+    assert bits_equal(dev, got)
+    monkeypatch.setenv("TILEFFT_NO_ROWS_PF", "1")
+    tf.tilefft._plan_cache.clear()
+    ref = tf.fft_tiled(x, tf.make_plan(n))
+    tf.tilefft._plan_cache.clear()
+    assert bits_equal(ref, got)
