@@ -339,8 +339,8 @@ struct SyncNamed {
 
 template <int LA, int LB, bool INV, int OUTT>
 struct TwoWsCfg {
-  // half-tile exchange buffer (2 rounds): a full one (1 round) leaves too little
-  // L1 for the twiddle tables and measured slower (618 vs 585 us, 8192^2)
+  // half-tile exchange buffer (2 rounds): a full one (1 round, 192 KB of shared
+  // memory) measured slower twice (618 vs 585 us, then 612 vs 536 us at 8192^2)
   using Base = TwoCfg<LA, LB, INV, OUTT, 2>;
   static constexpr int NS = 2;  // A tile slots
   // (exchanging in place in the consumed tile slot -- one round, slot refilled
