@@ -47,6 +47,16 @@ CONFIGS = {
 }
 
 
+# device pass factorisation each config's default plan executes (asserted by tests/test_gpu_bench_plans.py)
+DEVICE_FACTORS = {
+    "batched1024": [1024],
+    "1d_2e20": [1024, 1024],
+    "1d_2e26": [512, 512, 256],
+    "2d_8192": [8192, 8192],
+    "1d_2e30": [1024, 1024, 1024],
+}
+
+
 def splitmix_signal(count: int, seed: int = 1) -> np.ndarray:
     """Counter-based uniform(-1,1) complex64 input; identical to
     the oracle's orc_splitmix_signal_f32, vectorised."""
@@ -150,6 +160,16 @@ def dist_env():
 def flops_per_transform(n: int, kind: str) -> float:
     total = n * n if kind == "2d" else n
     return 5.0 * total * math.log2(total)
+
+
+def make_device_plan(config: str, device: int = 0, batch=None):
+    """The plan bench.py times for `config` (tests/test_gpu_bench_plans.py pins its parity)."""
+    from paper_1707_07263_b200 import _capi
+    n, b, kind, _, _ = CONFIGS[config]
+    b = b if batch is None else batch
+    if kind == "2d":
+        return _capi.DevicePlan.create_2d(n, n, b, 8, device)
+    return _capi.DevicePlan.create(n, b, None, 8, _capi.MODE_FAST, None, device)
 
 
 # ---------------------------------------------------------------------------------------------------
@@ -298,10 +318,7 @@ def main():
         def step():
             dfft.forward(x, y)
     else:
-        if kind == "2d":
-            plan = _capi.DevicePlan.create_2d(n, n, batch, 8, dev)
-        else:
-            plan = _capi.DevicePlan.create(total, batch, None, 8, _capi.MODE_FAST, None, dev)
+        plan = make_device_plan(args.config, dev)
         info = plan.info()
         elems = total * batch
         host_in = splitmix_signal(elems, seed=1 + rank)

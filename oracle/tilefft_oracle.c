@@ -330,3 +330,93 @@ void orc_splitmix_signal_f32(uint64_t n, uint64_t seed, float* out) {
     out[i] = (float)(u * 2.0 - 1.0);
   }
 }
+
+/* Exact spectrum bins of a large fp32 signal, for parity at sizes where an
+ * O(N^2) DFT is out of reach ("16 sampled bins against a direct
+ * fp64 O(N) sum" at 2^30). out[2b..2b+1] = sum_n x[n] * exp(sign*2*pi*i*n*k_b/N)
+ * accumulated in fp64 per thread chunk; the root W^((n*k) mod N) is the
+ * product of a coarse and a fine fp64 table entry (each from cos/sin of the
+ * exact angle), so the error per term is a few fp64 ulps. This is the
+ * definition of the DFT (reference_dft.hpp:41-60), not a transcription of
+ * its loop (which is O(N^2) and fp64-input). */
+#include <pthread.h>
+typedef struct {
+  const float* x;
+  uint64_t n, begin, end, k;
+  int sign, fb;
+  const double* coarse;
+  const double* fine;
+  double re, im;
+} orc_bin_job;
+
+static void* orc_bin_worker(void* arg) {
+  orc_bin_job* j = (orc_bin_job*)arg;
+  const uint64_t mask = j->n - 1, fmask = (1ull << j->fb) - 1;
+  double sre = 0, sim = 0;
+  uint64_t e = (j->begin * j->k) & mask;
+  for (uint64_t i = j->begin; i < j->end; ++i) {
+    const double* c = j->coarse + 2 * (e >> j->fb);
+    const double* f = j->fine + 2 * (e & fmask);
+    const double wr = c[0] * f[0] - c[1] * f[1];
+    const double wi = (c[0] * f[1] + c[1] * f[0]) * (double)j->sign;
+    const double xr = (double)j->x[2 * i], xi = (double)j->x[2 * i + 1];
+    sre += xr * wr - xi * wi;
+    sim += xr * wi + xi * wr;
+    e = (e + j->k) & mask;
+  }
+  j->re = sre;
+  j->im = sim;
+  return 0;
+}
+
+int orc_dft_bins_f32in(const float* x, uint64_t n, const uint64_t* bins, uint32_t nbins, int sign, uint32_t threads,
+                       double* out) {
+  if (!is_pow2(n) || n < 2 || threads == 0) return -1;
+  const uint32_t lm = log2_exact(n);
+  const int fb = (int)((lm + 1) / 2);
+  const uint64_t nf = 1ull << fb, nc = n >> fb;
+  double* coarse = (double*)malloc(2 * nc * sizeof(double));
+  double* fine = (double*)malloc(2 * nf * sizeof(double));
+  orc_bin_job* jobs = (orc_bin_job*)calloc(threads, sizeof(orc_bin_job));
+  pthread_t* tid = (pthread_t*)calloc(threads, sizeof(pthread_t));
+  if (!coarse || !fine || !jobs || !tid) return -1;
+  for (uint64_t i = 0; i < nc; ++i) {  /* exp(+2 pi i * i*nf / n) (sign applied per term) */
+    const double a = 2.0 * kPi * (double)(i * nf) / (double)n;
+    coarse[2 * i] = cos(a);
+    coarse[2 * i + 1] = sin(a);
+  }
+  for (uint64_t i = 0; i < nf; ++i) {
+    const double a = 2.0 * kPi * (double)i / (double)n;
+    fine[2 * i] = cos(a);
+    fine[2 * i + 1] = sin(a);
+  }
+  for (uint32_t b = 0; b < nbins; ++b) {
+    const uint64_t per = (n + threads - 1) / threads;
+    for (uint32_t t = 0; t < threads; ++t) {
+      orc_bin_job* j = &jobs[t];
+      j->x = x;
+      j->n = n;
+      j->begin = (uint64_t)t * per < n ? (uint64_t)t * per : n;
+      j->end = j->begin + per < n ? j->begin + per : n;
+      j->k = bins[b] & (n - 1);
+      j->sign = sign < 0 ? -1 : 1;
+      j->fb = fb;
+      j->coarse = coarse;
+      j->fine = fine;
+      pthread_create(&tid[t], 0, orc_bin_worker, j);
+    }
+    double re = 0, im = 0;
+    for (uint32_t t = 0; t < threads; ++t) {
+      pthread_join(tid[t], 0);
+      re += jobs[t].re;
+      im += jobs[t].im;
+    }
+    out[2 * b] = re;
+    out[2 * b + 1] = im;
+  }
+  free(coarse);
+  free(fine);
+  free(jobs);
+  free(tid);
+  return 0;
+}

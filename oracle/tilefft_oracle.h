@@ -71,6 +71,11 @@ void orc_random_signal(uint64_t n, uint64_t seed, double* out);
  * re = u(splitmix64(seed, 2i)), im = u(splitmix64(seed, 2i+1)), u in [-1,1). */
 void orc_splitmix_signal_f32(uint64_t n, uint64_t seed, float* out);
 
+/* Exact fp64 DFT bins of an fp32 signal (sign -1 forward), `threads` POSIX
+ * threads; for sampled-bin parity at 2^30. */
+int orc_dft_bins_f32in(const float* x, uint64_t n, const uint64_t* bins, uint32_t nbins, int sign, uint32_t threads,
+                       double* out);
+
 #ifdef __cplusplus
 }
 #endif

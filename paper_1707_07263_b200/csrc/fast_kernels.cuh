@@ -234,7 +234,6 @@ struct RowsCfg {
 template <typename Real, int L, int FPC, bool INV>
 __global__ void __launch_bounds__(RowsCfg<Real, L, FPC>::THREADS)
 k_rows(const C2<Real>* in, C2<Real>* out, long long nrows, const C2<Real>* __restrict__ tw, Real scale) {
-  pdl_enter();
   using Cfg = RowsCfg<Real, L, FPC>;
   using V = C2<Real>;
   using Sh = typename Cfg::Sh;
@@ -304,7 +303,6 @@ struct RowsTmaCfg {
 template <typename Real, int L, int WARPS, int S, bool INV, bool TWS = false>
 __global__ void __launch_bounds__(WARPS * 32)
 k_rows_tma(const C2<Real>* in, C2<Real>* out, long long nrows, const C2<Real>* __restrict__ tw_g, Real scale) {
-  pdl_enter();
   using Cfg = RowsTmaCfg<Real, L, WARPS, S>;
   using V = C2<Real>;
   using Sh = typename Cfg::Sh;
@@ -506,7 +504,6 @@ template <typename Real, int L, bool INV, bool TWID, int MODE, int F_ = FOf<Real
 __global__ void __launch_bounds__(CombCfg<Real, L, F_>::THREADS, CombCfg<Real, L, F_>::MINB)
 k_comb(const C2<Real>* in, C2<Real>* out, CombArgs a, const C2<Real>* __restrict__ tw,
        const double2* __restrict__ wc, const double2* __restrict__ wf, Real scale) {
-  pdl_enter();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   comb_tile<Real, L, INV, TWID, MODE, F_>(in, out, a, tw, wc, wf, scale, blockIdx.x,
                                           reinterpret_cast<C2<Real>*>(smem_raw));
@@ -578,7 +575,6 @@ template <typename Real, int L, bool INV, bool TWID, int MODE, int F_ = FOf<Real
 __global__ void __launch_bounds__(CombTmaCfg<Real, L, F_>::THREADS, CombTmaCfg<Real, L, F_>::MINB)
 k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs a, const C2<Real>* __restrict__ tw,
            const double2* __restrict__ wc, const double2* __restrict__ wf, Real scale) {
-  pdl_enter();
   using Cfg = CombTmaCfg<Real, L, F_>;
   using V = C2<Real>;
   using Sh = typename Cfg::Sh;
@@ -774,7 +770,6 @@ __device__ __forceinline__ void final_tile(const C2<Real>* in, C2<Real>* out, co
 template <typename Real, int L, bool INV, int F_ = FOf<Real>::v>
 __global__ void __launch_bounds__(FinalCfg<Real, L, F_>::THREADS, FinalCfg<Real, L, F_>::THREADS <= 256 ? 2 : 1)
 k_final_t(const C2<Real>* in, C2<Real>* out, FinalArgs a, const C2<Real>* __restrict__ tw, Real scale) {
-  pdl_enter();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   final_tile<Real, L, INV, F_>(in, out, a, tw, scale, blockIdx.x, reinterpret_cast<C2<Real>*>(smem_raw));
 }
@@ -799,7 +794,6 @@ template <int L, bool INV>
 __global__ void __launch_bounds__(RowsPfCfg<L>::THREADS, 2)
 k_rows_pf(const float2* __restrict__ in, float2* __restrict__ out, long long nrows, const float2* __restrict__ tw,
           float scale) {
-  pdl_enter();
   using Cfg = RowsPfCfg<L>;
   using V = float2;
   using Sh = typename Cfg::Sh;

@@ -8,8 +8,6 @@
 #include "exact_kernels.cuh"
 #include "fast_kernels.cuh"
 #include "twolevel.cuh"
-#include "comb_w.cuh"
-#include "small_fused.cuh"
 #include "../../include/tilefft_b200.h"
 
 namespace tfb_host {
@@ -26,7 +24,7 @@ int fail(int code, const char* fmt, ...);
 // Opt a kernel into >48 KB dynamic shared memory (once per function/device).
 int ensure_smem(const void* fn, int bytes);
 
-enum PassKind { K_ROWS = 0, K_COMB1D = 1, K_COMBAX = 2, K_FINALT = 3, K_EXACT = 4, K_BITREV = 5, K_LEVEL = 6, K_TWO = 7, K_SMALL2 = 8 };
+enum PassKind { K_ROWS = 0, K_COMB1D = 1, K_COMBAX = 2, K_FINALT = 3, K_EXACT = 4, K_BITREV = 5, K_LEVEL = 6, K_TWO = 7 };
 
 struct Pass {
   PassKind kind;
@@ -51,12 +49,6 @@ struct Pass {
   long long two_cols, two_es_in;  // columns along the axis and their element stride (input)
   size_t twl_off;                 // W_L^e table (L entries)
   int two_ctas;                   // persistent grid
-  // K_SMALL2 (small_fused.cuh): comb pass (comb, L, tw_off, wc/wf) + final pass
-  // (fin, L2, tw2_off) of a 2-pass plan in one launch
-  int L2;
-  size_t tw2_off;
-  void* work_p;                   // the plan workspace (pass-1 output)
-  unsigned* gbar;                 // tile counters (2 x u64)
 };
 
 // Distributed four-step, pass 1 on one rank (see tilefft_dist_* in the C ABI).

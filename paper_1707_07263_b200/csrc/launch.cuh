@@ -43,11 +43,11 @@ constexpr int kRowsWarps = 4;
 constexpr int kRowsStages = 2;
 
 // one persistent TMA rows launch with W warps per CTA and an S-deep ring per warp
-template <typename Real, int L, bool INV, int W, int S, bool TWS>
+template <typename Real, int L, bool INV, int W, int S>
 int launch_rows_tma(const Pass& ps, const void* in, void* out, const void* tw, Real scale, cudaStream_t st) {
   using Cfg = tfb::RowsTmaCfg<Real, L, W, S>;
-  auto k = tfb::k_rows_tma<Real, L, W, S, INV, TWS>;
-  const int smem = Cfg::SMEM + (TWS ? Cfg::TW_BYTES : 0);
+  auto k = tfb::k_rows_tma<Real, L, W, S, INV>;
+  const int smem = Cfg::SMEM;
   if (int rc = ensure_smem((const void*)k, smem)) return rc;
   static int blocks_per_sm[16] = {};
   int dev = 0;
@@ -73,16 +73,13 @@ int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, const
   const bool aligned = ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0) && (L * sizeof(tfb::C2<Real>)) % 16 == 0;
   if constexpr (T <= 32) {
     if (aligned && !ps.no_tma) {
-      // TILEFFT_TW_SMEM=1: stage roots from shared memory instead of the read-only path (measurement switch)
-      if (tfb::Shape<L, RM>::NST > 1 && env_int_or("TILEFFT_TW_SMEM", 0))
-        return launch_rows_tma<Real, L, INV, kRowsWarps, kRowsStages, true>(ps, in, out, tw, scale, st);
-      // (4 warps x 2-deep rings measured best on batched 1024 x 65536: 0.174 ms; 4x3 0.199, 2x3 0.201,
-      // 2x4 0.196, 8x2 0.195, 1x4 0.187, 1x6 0.242 -- profiles/r01_s3_rows_tma_sweep.txt)
-      return launch_rows_tma<Real, L, INV, kRowsWarps, kRowsStages, false>(ps, in, out, tw, scale, st);
+      // stage roots through the read-only path, not shared memory (measured:
+      // profiles/r02_twiddle_ab.txt, tools/microbench/twiddle_ab.cu);
+      return launch_rows_tma<Real, L, INV, kRowsWarps, kRowsStages>(ps, in, out, tw, scale, st);
     }
   }
   if constexpr (std::is_same<Real, float>::value && L >= 2048) {
-    if (aligned && !ps.no_tma && !env_set("TILEFFT_NO_ROWS_PF")) {
+    if (aligned && !ps.no_tma) {
       using CfgP = tfb::RowsPfCfg<L>;
       auto k = tfb::k_rows_pf<L, INV>;
       if (int rc = ensure_smem((const void*)k, CfgP::SMEM)) return rc;
@@ -117,21 +114,6 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   }();
   return fn;
-}
-
-// The warp-owned comb kernel (comb_w.cuh) is opt-in: measured slower than
-// K_COMB_TMA at 2^26 (0.78 vs 0.66 ms; 8 consumer warps per SM leave the
-// twiddle and exchange latencies exposed).
-inline bool comb_w_disabled() {
-  const char* e = std::getenv("TILEFFT_COMBW");
-  return !(e && *e && *e != '0');
-}
-
-
-// Two-level passes use the warp-specialised kernel unless TILEFFT_TWO_WS=0.
-inline bool two_ws_enabled() {
-  const char* e = std::getenv("TILEFFT_TWO_WS");
-  return !(e && *e == '0');
 }
 
 // Strided comb tile as a 4-D tensor {column (8-byte words), n, rr, group}.
@@ -171,79 +153,6 @@ bool encode_comb_map(CUtensorMap* map, const Pass& ps, const void* in) {
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
-}
-
-// Warp-owned comb pass (comb_w.cuh): fp32, 64 <= L <= 512, F = 8192 / L
-// adjacent combs per tile. Returns 1 when the geometry does not fit (the
-// caller then uses K_COMB_TMA / K_COMB).
-template <int L, bool INV>
-int launch_comb_w(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, float scale,
-                  cudaStream_t st) {
-  using Cfg = tfb::CombWCfg<L>;
-  constexpr int F = Cfg::F;
-  auto enc = tensor_map_encoder();
-  const tfb::CombArgs& c = ps.comb;
-  const bool ax = ps.kind == K_COMBAX;
-  const long long ncols = ax ? c.es : c.rps;
-  if (!enc || ((uintptr_t)in % 16) || ((uintptr_t)out % 16) || ncols % F) return 1;
-  const long long B = c.ntiles / (c.chunks * c.groups_per_batch);
-  tfb::CombTmaArgs a{};
-  a.chunks = ncols / F;
-  a.groups_per_batch = c.groups_per_batch;
-  a.ntiles = a.chunks * c.groups_per_batch * B;
-  a.rps = c.rps;
-  a.sub_len = c.sub_len;
-  a.es = c.es;
-  a.bstride = c.bstride;
-  a.out_w_last = c.out_w_last;
-  a.final_pass = c.final_pass;
-  a.fvalid = F;
-  a.fb = c.fb;
-  a.p = c.p;
-  a.m_mask = c.m_mask;
-  for (int i = 0; i < 8; ++i) {
-    a.out_w[i] = c.out_w[i];
-    a.sub_w[i] = c.sub_w[i];
-  }
-  cuuint64_t di[4], si[3], dout[4], so[3];
-  if (!ax) {
-    di[0] = (cuuint64_t)c.rps; di[1] = L; di[2] = 1; di[3] = (cuuint64_t)(B * c.groups_per_batch);
-    si[0] = (cuuint64_t)(c.rps * 8); si[1] = (cuuint64_t)(c.sub_len * 8); si[2] = si[1];
-    for (int i = 0; i < 4; ++i) dout[i] = di[i];
-    for (int i = 0; i < 3; ++i) so[i] = si[i];
-  } else {
-    di[0] = (cuuint64_t)c.es; di[1] = L; di[2] = (cuuint64_t)c.rps; di[3] = (cuuint64_t)(B * (c.groups_per_batch / c.rps));
-    si[0] = (cuuint64_t)(c.rps * c.es * 8); si[1] = (cuuint64_t)(c.es * 8); si[2] = (cuuint64_t)(c.sub_len * c.es * 8);
-    if (c.final_pass) {
-      dout[0] = (cuuint64_t)c.es; dout[1] = L; dout[2] = (cuuint64_t)c.out_w_last; dout[3] = (cuuint64_t)B;
-      so[0] = (cuuint64_t)(c.out_w_last * c.es * 8); so[1] = (cuuint64_t)(c.es * 8); so[2] = (cuuint64_t)(c.bstride * 8);
-    } else {
-      for (int i = 0; i < 4; ++i) dout[i] = di[i];
-      for (int i = 0; i < 3; ++i) so[i] = si[i];
-    }
-  }
-  for (int i = 0; i < 3; ++i)
-    if (si[i] % 16 || so[i] % 16 || si[i] >= (1ull << 40) || so[i] >= (1ull << 40)) return 1;
-  const cuuint32_t box[4] = {16, (cuuint32_t)Cfg::BL, 1, 1};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUtensorMap mi, mo;
-  if (enc(&mi, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(in), di, si, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
-      enc(&mo, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, out, dout, so, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return 1;
-  auto go = [&](auto k) -> int {
-    if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return -rc;
-    const long long grid = std::max<long long>(1, std::min<long long>(a.ntiles, (long long)sm_count()));
-    k<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, st>>>(mi, mo, a, (const float2*)tb + ps.tw_off,
-                                                      (const double2*)tb64 + ps.wc_off, (const double2*)tb64 + ps.wf_off,
-                                                      scale);
-    if (cudaGetLastError() != cudaSuccess) return -fail(TILEFFT_ECUDA, "k_comb_w launch failed");
-    return 0;
-  };
-  if (!ax) return go(tfb::k_comb_w<L, INV, true, 0>);
-  if (ps.twid) return go(tfb::k_comb_w<L, INV, true, 1>);
-  return go(tfb::k_comb_w<L, INV, false, 1>);
 }
 
 // Persistent TMA-pipelined comb pass (K_COMB_TMA) with F-comb tiles.
@@ -289,12 +198,6 @@ int launch_comb_tma(const Pass& ps, const CUtensorMap& map, void* out, const voi
 template <typename Real, int L, bool INV>
 int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, Real scale,
                 cudaStream_t st) {
-  if constexpr (std::is_same<Real, float>::value && L >= 64 && L <= 512) {
-    if (!ps.no_tma && !comb_w_disabled()) {
-      const int rc = launch_comb_w<L, INV>(ps, in, out, tb, tb64, scale, st);
-      if (rc <= 0) return -rc;
-    }
-  }
   using V = tfb::C2<Real>;
   const V* t = (const V*)tb;
   const double2* t64 = (const double2*)tb64;
@@ -302,7 +205,7 @@ int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, const
   // 4-comb tiles spread the pass over every SM
   if constexpr (std::is_same<Real, float>::value && L >= 64) {
     constexpr int FS = 4;
-    if (ps.kind == K_COMB1D && ps.comb.ntiles < 2LL * sm_count() && ps.comb.rps % 16 == 0 && !env_set("TILEFFT_NO_SMALLF")) {
+    if (ps.kind == K_COMB1D && ps.comb.ntiles < 2LL * sm_count() && ps.comb.rps % 16 == 0) {
       using CfgS = tfb::CombCfg<float, L, FS>;
       tfb::CombArgs a = ps.comb;
       a.chunks *= 16 / FS;
@@ -346,7 +249,7 @@ int launch_final(const Pass& ps, const void* in, void* out, const void* tb, cons
   using V = tfb::C2<Real>;
   if constexpr (std::is_same<Real, float>::value && L >= 64) {
     constexpr int FS = 4;
-    if (ps.fin.ntiles < 2LL * sm_count() && !env_set("TILEFFT_NO_SMALLF")) {
+    if (ps.fin.ntiles < 2LL * sm_count()) {
       using CfgS = tfb::FinalCfg<float, L, FS>;
       tfb::FinalArgs a = ps.fin;
       a.chunks *= 16 / FS;
@@ -395,30 +298,13 @@ int launch_two_k(const Pass& ps, const void* in, void* out, const void* tb, cons
     return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled failed for the two-level pass");
   const float2* t = (const float2*)tb;
   const double2* t64 = (const double2*)tb64;
-  if (two_ws_enabled()) {
-    // warp-specialised variant: one 512-thread CTA per SM (A team + B team)
-    using WCfg = tfb::TwoWsCfg<LA, LB, INV, OUTT>;
-    auto kw = tfb::k_two_ws<LA, LB, INV, OUTT, TWID>;
-    if (int rc = ensure_smem((const void*)kw, WCfg::SMEM)) return rc;
-    CUDA_TRY(cudaMemsetAsync(a.ctrl, 0, sizeof(unsigned) * (2 + 2 * a.nslot), st));
-    kw<<<sm_count(), 512, WCfg::SMEM, st>>>(map, (float2*)out, a, t + ps.tw_off, t + ps.twl_off, t64 + ps.wc_off,
-                                             t64 + ps.wf_off, scale);
-    CUDA_TRY(cudaGetLastError());
-    return 0;
-  }
-  auto k = tfb::k_two<LA, LB, INV, OUTT, TWID>;
-  if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
-  static int occ[16] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!occ[dev & 15]) {
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev & 15], k, 256, Cfg::SMEM));
-    if (occ[dev & 15] < 1) return fail(TILEFFT_ECUDA, "two-level pass: kernel does not fit on an SM");
-  }
-  const int grid = sm_count() * occ[dev & 15];
-  CUDA_TRY(cudaMemsetAsync(a.ctrl, 0, sizeof(unsigned) * (1 + 2 * a.nslot), st));
-  k<<<grid, 256, Cfg::SMEM, st>>>(map, (float2*)out, a, t + ps.tw_off, t + ps.twl_off, t64 + ps.wc_off,
-                                  t64 + ps.wf_off, scale);
+  // warp-specialised two-level kernel: one 512-thread CTA per SM (A team + B team)
+  using WCfg = tfb::TwoWsCfg<LA, LB, INV, OUTT>;
+  auto kw = tfb::k_two_ws<LA, LB, INV, OUTT, TWID>;
+  if (int rc = ensure_smem((const void*)kw, WCfg::SMEM)) return rc;
+  CUDA_TRY(cudaMemsetAsync(a.ctrl, 0, sizeof(unsigned) * (2 + 2 * a.nslot), st));
+  kw<<<sm_count(), 512, WCfg::SMEM, st>>>(map, (float2*)out, a, t + ps.tw_off, t + ps.twl_off, t64 + ps.wc_off,
+                                           t64 + ps.wf_off, scale);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -449,75 +335,9 @@ int launch_two(const Pass& ps, const void* in, void* out, const void* tb, const 
   return fail(TILEFFT_EINVAL, "internal: no two-level kernel for %d x %d", ps.la, ps.lb);
 }
 
-// K_SMALL2: both passes of a small 2-pass fp32 plan in one launch. Returns 1
-// (nothing launched) when the kernel does not fit an SM, so the caller runs
-// the two passes as separate kernels.
-template <int L1, int L2, bool INV>
-int launch_small2_k(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, float scale,
-                    cudaStream_t st) {
-  using Cfg = tfb::Small2Cfg<L1, L2>;
-  auto k = tfb::k_small2<L1, L2, INV>;
-  if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
-  static int occ[16] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!occ[dev & 15]) {
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev & 15], k, Cfg::THREADS, Cfg::SMEM));
-    if (occ[dev & 15] < 1) occ[dev & 15] = -1;
-  }
-  if (occ[dev & 15] < 1) return 1;
-  tfb::CombArgs a1 = ps.comb;
-  a1.chunks *= 16 / Cfg::F1;
-  a1.ntiles *= 16 / Cfg::F1;
-  a1.fvalid = Cfg::F1;
-  tfb::FinalArgs a2 = ps.fin;
-  a2.chunks *= 16 / Cfg::F2;
-  a2.ntiles *= 16 / Cfg::F2;
-  const long long want = std::max(a1.ntiles, a2.ntiles);
-  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(want, (long long)occ[dev & 15] * sm_count()));
-  k<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>((const float2*)in, (float2*)ps.work_p, (float2*)out, a1, a2,
-                                           (const float2*)tb + ps.tw_off, (const float2*)tb + ps.tw2_off,
-                                           (const double2*)tb64 + ps.wc_off, (const double2*)tb64 + ps.wf_off, scale,
-                                           (unsigned long long*)ps.gbar);
-  CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
-template <bool INV>
-int launch_small2(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, float scale,
-                  cudaStream_t st) {
-  switch (ps.L * 10000 + ps.L2) {
-    case 128 * 10000 + 128: return launch_small2_k<128, 128, INV>(ps, in, out, tb, tb64, scale, st);
-    case 256 * 10000 + 128: return launch_small2_k<256, 128, INV>(ps, in, out, tb, tb64, scale, st);
-    case 256 * 10000 + 256: return launch_small2_k<256, 256, INV>(ps, in, out, tb, tb64, scale, st);
-    case 512 * 10000 + 256: return launch_small2_k<512, 256, INV>(ps, in, out, tb, tb64, scale, st);
-    case 512 * 10000 + 512: return launch_small2_k<512, 512, INV>(ps, in, out, tb, tb64, scale, st);
-    case 1024 * 10000 + 512: return launch_small2_k<1024, 512, INV>(ps, in, out, tb, tb64, scale, st);
-    case 1024 * 10000 + 1024: return launch_small2_k<1024, 1024, INV>(ps, in, out, tb, tb64, scale, st);
-  }
-  return 1;
-}
-
 template <typename Real, bool INV>
 int launch_fast(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, Real scale,
                 cudaStream_t st) {
-  if (ps.kind == K_SMALL2) {
-    if constexpr (std::is_same<Real, float>::value) {
-      const int rc = launch_small2<INV>(ps, in, out, tb, tb64, scale, st);
-      if (rc <= 0) return rc;
-    }
-    // no fused kernel for this shape: the same two passes as separate kernels
-    Pass p1 = ps, p2 = ps;
-    p1.kind = K_COMB1D;
-    p1.grid = ps.comb.ntiles;
-    p2.kind = K_FINALT;
-    p2.L = ps.L2;
-    p2.tw_off = ps.tw2_off;
-    p2.twid = false;
-    p2.grid = ps.fin.ntiles;
-    if (int rc = launch_fast<Real, INV>(p1, in, ps.work_p, tb, tb64, (Real)1, st)) return rc;
-    return launch_fast<Real, INV>(p2, ps.work_p, out, tb, tb64, scale, st);
-  }
 #define DISPATCH(FN, ...)                                                     \
   switch (ps.L) {                                                             \
     case 2: return FN<Real, 2, INV>(ps, in, out, tb, tb64, scale, st);              \

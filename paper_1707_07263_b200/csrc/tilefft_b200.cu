@@ -132,7 +132,6 @@ struct tilefft_plan_s {
   DevBuf work;            // workspace (batch * n elements)
   std::vector<Pass> passes_alt;  // same transform without two-level passes (used when the input is not 16-B aligned)
   DevBuf scratch, ctrl;   // two-level passes: L2-resident exchange slots and their counters
-  DevBuf gbar;            // K_SMALL2 tile counter + pass-1 done counter (64-bit, monotonic)
   // Replayed launch sequences: one CUDA graph per (in, out, sign), captured on
   // first use; a replay costs one cudaGraphLaunch instead of per-pass host work
   // (tensor-map encoding, occupancy queries, 2-3 launches).
@@ -146,6 +145,11 @@ struct tilefft_plan_s {
   std::vector<GraphEntry> graphs;
   std::mutex graph_mu;
   cudaStream_t cap_stream = nullptr;
+  // Every exec of the plan uses the same workspace, two-level scratch ring and
+  // counters, so execs on different streams are ordered on the device: each
+  // exec waits for the previous one (cudaStreamWaitEvent on this event, a
+  // no-op on the same stream) and records it when its last pass is queued.
+  cudaEvent_t exec_done = nullptr;
   size_t table_elems = 0;
   // host-path staging
   std::mutex host_mu;
@@ -167,6 +171,7 @@ struct tilefft_plan_s {
     if (inner) tilefft_plan_destroy(inner);
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (exec_done) cudaEventDestroy(exec_done);
     for (int i = 0; i < kHostStreams; ++i) {
       if (hs[i]) cudaStreamDestroy(hs[i]);
       if (hev[i]) cudaEventDestroy(hev[i]);
@@ -422,23 +427,6 @@ int build_fast_1d(tilefft_plan_s* P, TableBuilder<Real>& tb) {
   }
   P->dev_factors = f;
   if (build_two_1d<Real>(P, tb)) return 0;
-  // small (L2-resident) 2-pass fp32 plans: both passes in one launch. Opt-in
-  // (TILEFFT_FUSE=1): measured one 2.05 us step slower than two launches at
-  // every size 2^14..2^20 (16.4 vs 14.4 us at 2^20) -- the grab / release /
-  // acquire round trips between the passes cost more than the launch gap.
-  if (std::is_same<Real, float>::value && p == 2 && n * B <= (1ull << 21) && f[1] >= 128 &&
-      (f[0] == f[1] || f[0] == 2 * f[1]) && env_flag("TILEFFT_FUSE")) {
-    Pass fused = P->passes[0];
-    const Pass& fin = P->passes[1];
-    fused.kind = K_SMALL2;
-    fused.src = 0;
-    fused.dst = 1;
-    fused.final_pass = true;
-    fused.fin = fin.fin;
-    fused.L2 = fin.L;
-    fused.tw2_off = fin.tw_off;
-    P->passes.assign(1, fused);
-  }
   return 0;
 }
 
@@ -599,7 +587,7 @@ template <typename Real>
 int finish_plan(tilefft_plan_s* P, TableBuilder<Real>& tb) {
   // workspace when any pass touches it
   bool need_work = false;
-  for (const Pass& ps : P->passes) need_work |= (ps.src == 2 || ps.dst == 2 || ps.kind == K_SMALL2);
+  for (const Pass& ps : P->passes) need_work |= (ps.src == 2 || ps.dst == 2);
   for (const Pass& ps : P->passes_alt) need_work |= (ps.src == 2 || ps.dst == 2);
   size_t scratch_elems = 0;
   int ctrl_words = 0;
@@ -622,15 +610,6 @@ int finish_plan(tilefft_plan_s* P, TableBuilder<Real>& tb) {
     int rc = P->work.alloc(elems * sizeof(tfb::C2<Real>));
     if (rc) return rc;
   }
-  for (Pass& ps : P->passes)
-    if (ps.kind == K_SMALL2) {
-      if (!P->gbar.p) {
-        if (int rc = P->gbar.alloc(2 * sizeof(unsigned long long))) return rc;
-        CUDA_TRY(cudaMemset(P->gbar.p, 0, 2 * sizeof(unsigned long long)));
-      }
-      ps.work_p = P->work.p;
-      ps.gbar = (unsigned*)P->gbar.p;
-    }
   if (P->tb64 && !P->tb64->h.empty()) {
     int rc = P->tables64.alloc(P->tb64->h.size() * sizeof(double));
     if (rc) return rc;
@@ -734,6 +713,10 @@ int tilefft_plan_create(tilefft_plan_t* out, uint64_t n, uint64_t batch, const u
     }
     if (prod != n) return fail(TILEFFT_EINVAL, "fft_tiled: signal length does not match the plan");
   }
+  // fast-path inter-pass exponents r*k are reduced mod M <= n in 32-bit
+  // arithmetic (fast_kernels.cuh interpass_scale): exact for n <= 2^32 only
+  if (mode == TILEFFT_MODE_FAST && n > (1ull << 32))
+    return fail(TILEFFT_EINVAL, "tilefft_plan_create: fast mode supports n <= 2^32");
   if ((mode == TILEFFT_MODE_EXACT || mode == TILEFFT_MODE_PERMUTE) && f.empty())
     return fail(TILEFFT_EINVAL, "fft_tiled: empty plan");
   if ((mode == TILEFFT_MODE_EXACT || mode == TILEFFT_MODE_LEVELWISE) && tv != nullptr &&
@@ -782,6 +765,7 @@ int tilefft_plan_create_2d(tilefft_plan_t* out, uint64_t ny, uint64_t nx, uint64
   if (batch < 1) return fail(TILEFFT_EINVAL, "tilefft_plan_create_2d: batch must be >= 1");
   if (elem_bytes != 8 && elem_bytes != 16) return fail(TILEFFT_EINVAL, "tilefft_plan_create_2d: elem_bytes must be 8 or 16");
   if (nx > 8192) return fail(TILEFFT_EINVAL, "tilefft_plan_create_2d: rows longer than 8192 are not supported yet");
+  if (ny > (1ull << 32) / nx) return fail(TILEFFT_EINVAL, "tilefft_plan_create_2d: ny * nx must be <= 2^32");
   if (int rc = check_device(device)) return rc;
   tilefft_plan_s* P = new (std::nothrow) tilefft_plan_s();
   if (!P) return fail(TILEFFT_ENOMEM, "out of host memory");
@@ -835,42 +819,6 @@ int tilefft_plan_create_2d(tilefft_plan_t* out, uint64_t ny, uint64_t nx, uint64
   return 0;
 }
 
-namespace {
-// Programmatic dependent launch inside a captured plan: every kernel -> kernel
-// edge becomes a programmatic edge, so pass s+1 is launched while pass s
-// drains and waits (griddepcontrol.wait, pdl_enter in every fast kernel) for
-// its completion before reading. Only FAST plans, whose kernels all call
-// pdl_enter; memset nodes keep ordinary edges. Any failure leaves the graph
-// as captured (the replay is then just not overlapped).
-void make_programmatic(cudaGraph_t graph) {
-  size_t ne = 0;
-  if (cudaGraphGetEdges(graph, nullptr, nullptr, &ne) != cudaSuccess || ne == 0) {
-    cudaGetLastError();
-    return;
-  }
-  std::vector<cudaGraphNode_t> from(ne), to(ne);
-  if (cudaGraphGetEdges(graph, from.data(), to.data(), &ne) != cudaSuccess) {
-    cudaGetLastError();
-    return;
-  }
-  for (size_t i = 0; i < ne; ++i) {
-    cudaGraphNodeType a, b;
-    if (cudaGraphNodeGetType(from[i], &a) != cudaSuccess || cudaGraphNodeGetType(to[i], &b) != cudaSuccess) break;
-    if (a != cudaGraphNodeTypeKernel || b != cudaGraphNodeTypeKernel) continue;
-    if (cudaGraphRemoveDependencies(graph, &from[i], &to[i], 1) != cudaSuccess) break;
-    cudaGraphEdgeData ed{};
-    ed.from_port = cudaGraphKernelNodePortProgrammatic;
-    ed.type = cudaGraphDependencyTypeProgrammatic;
-    if (cudaGraphAddDependencies_v2(graph, &from[i], &to[i], &ed, 1) != cudaSuccess) {
-      cudaGetLastError();
-      cudaGraphAddDependencies(graph, &from[i], &to[i], 1);  // restore the plain edge
-      break;
-    }
-  }
-  cudaGetLastError();
-}
-}  // namespace
-
 int tilefft_exec_c2c(tilefft_plan_t P, const void* in, void* out, int sign, void* stream) {
   g_err.clear();
   if (!P) return fail(TILEFFT_EINVAL, "tilefft_exec_c2c: null plan");
@@ -883,12 +831,19 @@ int tilefft_exec_c2c(tilefft_plan_t P, const void* in, void* out, int sign, void
   auto direct = [&](cudaStream_t s) {
     return P->elem_bytes == 8 ? exec_impl<float>(P, in, out, sign, s) : exec_impl<double>(P, in, out, sign, s);
   };
-  if (env_flag("TILEFFT_NO_GRAPH")) return direct(st);
   std::lock_guard<std::mutex> lock(P->graph_mu);
+  if (!P->exec_done) CUDA_TRY(cudaEventCreateWithFlags(&P->exec_done, cudaEventDisableTiming));
+  CUDA_TRY(cudaStreamWaitEvent(st, P->exec_done, 0));
+  auto launched = [&](int rc) -> int {
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(P->exec_done, st));
+    return 0;
+  };
+  if (env_flag("TILEFFT_NO_GRAPH")) return launched(direct(st));
   for (auto& g : P->graphs)
     if (g.in == in && g.out == out && g.sign == sign) {
       CUDA_TRY(cudaGraphLaunch(g.exec, st));
-      return 0;
+      return launched(0);
     }
   // capture the pass sequence once on a private stream (the caller's stream
   // may be the legacy default stream, which cannot be captured)
@@ -902,10 +857,6 @@ int tilefft_exec_c2c(tilefft_plan_t P, const void* in, void* out, int sign, void
     return rc;
   }
   if (ce != cudaSuccess) return fail(TILEFFT_ECUDA, "stream capture failed: %s", cudaGetErrorString(ce));
-  // opt-in (TILEFFT_PDL=1): measured neutral with the implicit trigger at CTA exit
-  // (2^14..2^30, 8192^2 within noise) and mixed with an early trigger (2^16
-  // 10.2 -> 8.2 us, 2^20 14.3 -> 16.4 us, 2^30 11.84 -> 12.07 ms)
-  if (P->mode == TILEFFT_MODE_FAST && env_flag("TILEFFT_PDL")) make_programmatic(graph);
   cudaGraphExec_t exec = nullptr;
   const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
@@ -916,13 +867,17 @@ int tilefft_exec_c2c(tilefft_plan_t P, const void* in, void* out, int sign, void
   }
   P->graphs.push_back({in, out, sign, exec});
   CUDA_TRY(cudaGraphLaunch(exec, st));
-  return 0;
+  return launched(0);
 }
 
 int tilefft_exec_c2c_host(tilefft_plan_t P, const void* h_in, void* h_out, int sign) {
   g_err.clear();
   if (!P) return fail(TILEFFT_EINVAL, "tilefft_exec_c2c_host: null plan");
   if (!h_in || !h_out) return fail(TILEFFT_EINVAL, "tilefft_exec_c2c_host: null buffer");
+  if (sign != TILEFFT_FORWARD && sign != TILEFFT_INVERSE)
+    return fail(TILEFFT_EINVAL, "tilefft_exec_c2c_host: sign must be -1 or +1");
+  if (P->mode == TILEFFT_MODE_PERMUTE && sign != TILEFFT_FORWARD)
+    return fail(TILEFFT_EINVAL, "tilefft_exec_c2c_host: permute mode is forward only");
   std::lock_guard<std::mutex> lock(P->host_mu);
   CUDA_TRY(cudaSetDevice(P->device));
   const uint64_t per = P->n;  // elements per transform (2D: ny*nx)
@@ -982,16 +937,28 @@ int tilefft_exec_c2c_host(tilefft_plan_t P, const void* h_in, void* h_out, int s
     for (auto it = tail.rbegin(); it != tail.rend(); ++it) sizes.push_back(*it);
   }
   Pass ps = P->passes[0];
+  // on an error part-way through, copies may still be reading/writing the
+  // caller's buffers: drain every queue before returning
+  auto drain = [&](int rc) -> int {
+    for (int i = 0; i < 3; ++i) cudaStreamSynchronize(P->hs[i]);
+    cudaGetLastError();
+    return rc;
+  };
+#define HOST_TRY(expr)                                                                            \
+  do {                                                                                            \
+    cudaError_t e_ = (expr);                                                                      \
+    if (e_ != cudaSuccess) return drain(fail(TILEFFT_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_))); \
+  } while (0)
   uint64_t b0 = 0;
   for (uint64_t idx = 0; idx < sizes.size(); b0 += sizes[idx], ++idx) {
     const int bi = (int)(idx % NB);
     const uint64_t nb = sizes[idx];
     const size_t off = b0 * per * eb, bytes = nb * per * eb;
     void* buf = P->hbuf[bi].p;
-    if (idx >= (uint64_t)NB) CUDA_TRY(cudaStreamWaitEvent(P->hs[0], P->hev[bi], 0));  // buffer drained
-    CUDA_TRY(cudaMemcpyAsync(buf, (const char*)h_in + off, bytes, cudaMemcpyHostToDevice, P->hs[0]));
-    CUDA_TRY(cudaEventRecord(P->hev_in[bi], P->hs[0]));
-    CUDA_TRY(cudaStreamWaitEvent(P->hs[1], P->hev_in[bi], 0));
+    if (idx >= (uint64_t)NB) HOST_TRY(cudaStreamWaitEvent(P->hs[0], P->hev[bi], 0));  // buffer drained
+    HOST_TRY(cudaMemcpyAsync(buf, (const char*)h_in + off, bytes, cudaMemcpyHostToDevice, P->hs[0]));
+    HOST_TRY(cudaEventRecord(P->hev_in[bi], P->hs[0]));
+    HOST_TRY(cudaStreamWaitEvent(P->hs[1], P->hev_in[bi], 0));
     ps.nrows = (long long)nb;
     const bool inv = sign == TILEFFT_INVERSE;
     int rc;
@@ -1004,13 +971,14 @@ int tilefft_exec_c2c_host(tilefft_plan_t P, const void* h_in, void* h_out, int s
       rc = inv ? launch_fast<double, true>(ps, buf, buf, P->tables.p, nullptr, scale, P->hs[1])
                : launch_fast<double, false>(ps, buf, buf, P->tables.p, nullptr, scale, P->hs[1]);
     }
-    if (rc) return rc;
-    CUDA_TRY(cudaEventRecord(P->hev_k[bi], P->hs[1]));
-    CUDA_TRY(cudaStreamWaitEvent(P->hs[2], P->hev_k[bi], 0));
-    CUDA_TRY(cudaMemcpyAsync((char*)h_out + off, buf, bytes, cudaMemcpyDeviceToHost, P->hs[2]));
-    CUDA_TRY(cudaEventRecord(P->hev[bi], P->hs[2]));
+    if (rc) return drain(rc);
+    HOST_TRY(cudaEventRecord(P->hev_k[bi], P->hs[1]));
+    HOST_TRY(cudaStreamWaitEvent(P->hs[2], P->hev_k[bi], 0));
+    HOST_TRY(cudaMemcpyAsync((char*)h_out + off, buf, bytes, cudaMemcpyDeviceToHost, P->hs[2]));
+    HOST_TRY(cudaEventRecord(P->hev[bi], P->hs[2]));
   }
-  CUDA_TRY(cudaStreamSynchronize(P->hs[2]));
+  HOST_TRY(cudaStreamSynchronize(P->hs[2]));
+#undef HOST_TRY
   return 0;
 }
 
@@ -1230,7 +1198,6 @@ int tilefft_plan_info(tilefft_plan_t P, tilefft_plan_info_t* info) {
   info->mode = P->mode;
   info->is_2d = P->is2d;
   info->passes = (uint32_t)P->passes.size();
-  for (const Pass& ps : P->passes) info->passes += ps.kind == K_SMALL2;  // two passes, one launch
   for (size_t i = 0; i < P->dev_factors.size() && i < 16; ++i) info->factors[i] = P->dev_factors[i];
   info->launches_per_exec = (uint32_t)P->passes.size();
   info->workspace_bytes = P->work.bytes;

@@ -66,16 +66,4 @@ __device__ __forceinline__ void bulk_wait() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Programmatic dependent launch (the plan's graph turns kernel -> kernel edges
-// into programmatic ones): every fast kernel lets its successor start
-// launching as soon as all of its own CTAs are running, then waits for its
-// predecessor to complete (and its stores to be visible) before touching
-// global memory. Both are no-ops for an ordinary launch.
-__device__ __forceinline__ void pdl_enter() {
-#ifdef TILEFFT_PDL_EARLY_TRIGGER
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-}
-
 }  // namespace tfb

@@ -98,227 +98,6 @@ __device__ __forceinline__ void discard_l2(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 
-// Item hand-out order: supersteps j = 0 .. G + D - 1, superstep j holds the
-// LB A items of group j (if j < G) followed by the LB B items of group j - D
-// (if j >= D). Returns kind 0 = A, 1 = B, -1 = done.
-__device__ __forceinline__ int two_decode(long long id, long long G, int D, int LBv, long long& g, int& sub) {
-  const long long p1 = (long long)D * LBv;
-  if (id < p1) { g = id / LBv; sub = (int)(id % LBv); return 0; }
-  id -= p1;
-  const long long mid = (G - D) * 2 * LBv;
-  if (id < mid) {
-    const long long j = D + id / (2 * LBv);
-    const int p = (int)(id % (2 * LBv));
-    if (p < LBv) { g = j; sub = p; return 0; }
-    g = j - D; sub = p - LBv; return 1;
-  }
-  id -= mid;
-  if (id < p1) { g = G - D + id / LBv; sub = (int)(id % LBv); return 1; }
-  return -1;
-}
-
-// Tensor map (4-D, 8-byte elements): {column, n1 (stride es), n2 (stride LB*es), batch}.
-// OUTT=1 tiles are loaded with the 128-byte swizzle: element (n2, f) lives at
-// row n2, 16-byte chunk (f/2) ^ (n2 & 7).
-template <int LA, int LB, bool INV, int OUTT, bool TWID>
-__global__ void __launch_bounds__(256, 2)
-k_two(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, TwoArgs a, const float2* __restrict__ tw,
-      const float2* __restrict__ twl, const double2* __restrict__ wc, const double2* __restrict__ wf, float scale) {
-  pdl_enter();
-  using Cfg = TwoCfg<LA, LB, INV, OUTT>;
-  using V = float2;
-  using Sh = typename Cfg::Sh;
-  constexpr int F = Cfg::F, T = Cfg::T, KB = Cfg::KB;
-  extern __shared__ unsigned char smem_raw[];
-  // align by pointer arithmetic: an integer round trip would lose the shared
-  // address space and turn every tile access into a generic LD.E/ST.E
-  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  V* tile = reinterpret_cast<V*>(base);
-  V* xb = tile + Cfg::TILE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(xb + Cfg::XB);
-  const int tid = threadIdx.x;
-  const long long G = a.groups;
-  const int D = a.D;
-  unsigned* doneA = a.ctrl + 1;
-  unsigned* doneB = a.ctrl + 1 + a.nslot;
-  __shared__ long long s_next_g;
-  __shared__ int s_next_kind, s_next_sub;
-  unsigned* work = a.ctrl;
-
-  if (tid == 0) {
-    mbar_init(full, 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-
-  auto issue = [&](long long g, int n1) {
-    const long long b = g / a.chunks, ch = g % a.chunks;
-    mbar_arrive_expect_tx(full, Cfg::TILE_BYTES);
-#pragma unroll 1
-    for (int r = 0; r < LA; r += Cfg::BL)
-      tma_load_4d_l2(tile + r * F, &tmap, (int)(ch * F), n1, r, (int)b, full);
-  };
-  // take the next item from the global counter; if it is an A item, start
-  // its tile load right away (the tile is free whenever this is called)
-  auto grab = [&]() {
-    long long g = 0;
-    int sub = 0;
-    const long long id = (long long)atomicAdd(work, 1u);
-    const int kind = two_decode(id, G, D, LB, g, sub);
-    if (kind == 0) issue(g, sub);
-    s_next_g = g;
-    s_next_kind = kind;
-    s_next_sub = sub;
-  };
-
-  if (tid == 0) grab();
-  __syncthreads();
-  long long g = s_next_g;
-  int kind = s_next_kind, sub = s_next_sub;
-  uint32_t phase = 0;
-
-#pragma unroll 1
-  while (kind >= 0) {
-    const int slot = (int)(g % a.nslot);
-    const unsigned gen = (unsigned)(g / a.nslot);
-    V* scr = reinterpret_cast<V*>(a.scratch) + (size_t)slot * Cfg::GROUP;
-    if (kind == 0) {
-      // ------------------------------------------------------------ A item
-      const int n1 = sub;
-      mbar_wait(full, phase);
-      phase ^= 1;
-      V v[Sh::R];
-      int t, f;
-      if constexpr (OUTT == 0) {
-        f = tid % F;
-        t = tid / F;
-#pragma unroll
-        for (int q = 0; q < Sh::R; ++q) v[q] = tile[(t + q * T) * F + f];
-      } else {
-        f = tid / T;
-        t = tid % T;
-#pragma unroll
-        for (int q = 0; q < Sh::R; ++q) {
-          const int n2 = t + q * T;
-          v[q] = tile[n2 * F + ((((f >> 1) ^ (n2 & 7))) << 1) + (f & 1)];
-        }
-      }
-      const int my_round = f / Cfg::FX, fx = f % Cfg::FX;
-      fence_proxy_async_smem();
-      __syncthreads();  // tile consumed
-      if (tid == 0) grab();
-      SyncBlock sy;
-      if constexpr (OUTT == 0) {
-        auto ex = [xb, fx](int i) -> V& { return xb[i * Cfg::FX + fx]; };
-        Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
-      } else {
-        V* reg = xb + fx * Cfg::REG;
-        auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
-        Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
-      }
-      // W_L^{n1 k2}
-#pragma unroll
-      for (int j = 0; j < Sh::R; ++j) {
-        const int k2 = out_index<LA, 32>(t, j);
-        v[j] = ctw<INV>(v[j], __ldg(twl + n1 * k2));
-      }
-      // the slot's previous group must be fully consumed
-      if (tid == 0 && gen > 0) wait_geq(doneB + slot, gen * LB);
-      __syncthreads();
-      if constexpr (OUTT == 0) {
-#pragma unroll
-        for (int j = 0; j < Sh::R; ++j) scr[((size_t)n1 * LA + out_index<LA, 32>(t, j)) * F + f] = v[j];
-      } else {
-#pragma unroll
-        for (int j = 0; j < Sh::R; ++j) scr[((size_t)n1 * F + f) * LA + out_index<LA, 32>(t, j)] = v[j];
-      }
-      __syncthreads();
-      if (tid == 0) {
-        signal_release(doneA + slot);
-      }
-    } else {
-      // ------------------------------------------------------------ B item
-      const int kb = sub;
-      if (tid == 0) {
-        grab();
-        wait_geq(doneA + slot, (gen + 1) * LB);
-      }
-      __syncthreads();
-      const long long b = g / a.chunks, ch = g % a.chunks;
-#pragma unroll
-      for (int m = 0; m < Cfg::PAIRS; ++m) {
-        // pair p = (k2l, f): lanes run along f (OUTT=0) or along k2 (OUTT=1)
-        const int p = tid + 256 * m;
-        int f, k2l;
-        if constexpr (OUTT == 0) {
-          f = p % F;
-          k2l = p / F;
-        } else {
-          k2l = p % KB;
-          f = p / KB;
-        }
-        const int k2 = kb * KB + k2l;
-        V v[LB];
-#pragma unroll
-        for (int n1 = 0; n1 < LB; ++n1) {
-          const V* q = OUTT == 0 ? scr + ((size_t)n1 * LA + k2) * F + f : scr + ((size_t)n1 * F + f) * LA + k2;
-          v[n1] = __ldcg(q);
-        }
-        reg_dft<LB, INV>(v);
-        const long long c = ch * F + f;  // column (comb) index
-        if constexpr (TWID) {
-          // W_M^{c (k2 + LA k1)} = W^{c k2} * (W^{c LA})^{k1}, powers in fp64
-          double2 w = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)k2) & a.m_mask, a.fb);
-          const double2 st = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)LA) & a.m_mask, a.fb);
-#pragma unroll
-          for (int k1 = 0; k1 < LB; ++k1) {
-            v[k1] = ctw<INV>(v[k1], make_float2((float)w.x, (float)w.y));
-            if (k1 + 1 < LB) w = cmul(w, st);
-          }
-        }
-        if (scale != 1.0f) {
-#pragma unroll
-          for (int k1 = 0; k1 < LB; ++k1) v[k1] = mk(v[k1].x * scale, v[k1].y * scale);
-        }
-        if constexpr (OUTT == 0) {
-          V* o = out + b * a.bs_out + c;
-#pragma unroll
-          for (int k1 = 0; k1 < LB; ++k1) o[(long long)(k2 + LA * k1) * a.es_out] = v[k1];
-        } else {
-          V* o = out + b * a.bs_out + c * a.es_out + k2;
-#pragma unroll
-          for (int k1 = 0; k1 < LB; ++k1) o[LA * k1] = v[k1];
-        }
-      }
-      __syncthreads();  // all scratch reads of this item done
-      if (a.discard) {
-        // this item owns LB x KB x 16 elements = LB*KB*F*8/128 lines
-        constexpr int LINES = LB * KB * F * 8 / 128;
-        for (int i = tid; i < LINES; i += 256) {
-          const V* q;
-          if constexpr (OUTT == 0) {
-            const int n1 = i / KB, k2 = kb * KB + i % KB;  // one line = 16 combs of (n1, k2)
-            q = scr + ((size_t)n1 * LA + k2) * F;
-          } else {
-            constexpr int LPR = KB * 8 / 128;               // lines per (n1, f) row segment
-            const int row = i / LPR, part = i % LPR;        // row = n1 * F + f
-            q = scr + (size_t)row * LA + kb * KB + part * 16;
-          }
-          discard_l2(q);
-        }
-        __syncthreads();
-      }
-      if (tid == 0) {
-        signal_release(doneB + slot);
-      }
-    }
-    __syncthreads();
-    g = s_next_g;
-    kind = s_next_kind;
-    sub = s_next_sub;
-  }
-}
-
 // ---------------------------------------------------------------- K_TWO_WS
 // Warp-specialised K_TWO: one persistent CTA per SM holds an A team (warps
 // 0-7) and a B team (warps 8-15) with their own item counters and named
@@ -352,7 +131,6 @@ template <int LA, int LB, bool INV, int OUTT, bool TWID>
 __global__ void __launch_bounds__(512, 1)
 k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, TwoArgs a, const float2* __restrict__ tw,
          const float2* __restrict__ twl, const double2* __restrict__ wc, const double2* __restrict__ wf, float scale) {
-  pdl_enter();
   using Cfg = typename TwoWsCfg<LA, LB, INV, OUTT>::Base;
   constexpr int NS = TwoWsCfg<LA, LB, INV, OUTT>::NS;
   // Who applies W_L^{n1 k2}: the B team when it has spare time (no inter-pass

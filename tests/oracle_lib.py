@@ -61,6 +61,7 @@ class Oracle:
         L.orc_random_bench_signal.argtypes = [u64, u64, vp]
         L.orc_random_signal.argtypes = [u64, u64, vp]
         L.orc_splitmix_signal_f32.argtypes = [u64, u64, vp]
+        L.orc_dft_bins_f32in.argtypes = [vp, u64, vp, u32, ctypes.c_int, u32, vp]
         L.orc_bit_reverse.argtypes = [u64, u32]
         L.orc_bit_reverse.restype = u64
         L.orc_gather_source_index.argtypes = [ctypes.POINTER(OrcPlan), u32, u64, u64]
@@ -152,6 +153,17 @@ class Oracle:
         self.lib.orc_splitmix_signal_f32(n, seed, _ptr(out))
         return out
 
+    def dft_bins(self, x: np.ndarray, bins, inverse=False, threads=None) -> np.ndarray:
+        """Exact fp64 DFT bins X[k] of a complex64 signal (O(N) per bin, threaded)."""
+        x = np.ascontiguousarray(x, dtype=np.complex64)
+        b = np.ascontiguousarray(np.asarray(bins, dtype=np.uint64))
+        out = np.empty(len(b), dtype=np.complex128)
+        rc = self.lib.orc_dft_bins_f32in(_ptr(x), x.shape[-1], _ptr(b), len(b), 1 if inverse else -1,
+                                         int(threads or os.cpu_count() or 1), _ptr(out))
+        if rc != 0:
+            raise ValueError("dft_bins: invalid argument")
+        return out
+
 
 class Reference:
     """The reference itself (compiled headers). Raises if not built."""
@@ -196,6 +208,32 @@ class Reference:
             if rc != 0:
                 raise ValueError("fft_tiled: invalid argument")
         return out
+
+    def fft_tiled_batched(self, x, cap=1024, threads=None):
+        """fp32 rows of x (shape (batch, n)) through the reference's fft_tiled,
+        `threads` std::threads each calling fft_tiled(threads=1) (BASELINE.md §2)."""
+        x = np.ascontiguousarray(x, dtype=np.complex64)
+        n = x.shape[-1]
+        batch = x.size // n
+        out = np.empty_like(x)
+        ctx = self.lib.ref_ctx_create(n, cap)
+        if not ctx:
+            raise ValueError("fft_tiled: invalid argument")
+        try:
+            self.lib.ref_ctx_exec_batched(ctx, _ptr(x), _ptr(out), batch, int(threads or os.cpu_count() or 1))
+        finally:
+            self.lib.ref_ctx_destroy(ctx)
+        return out
+
+    def fft2(self, img, cap=1024, threads=None):
+        """fp32 2D transform as rows then columns through fft_tiled (BASELINE.md §2 recipe;
+        the reference has no 2D entry point)."""
+        ny, nx = img.shape[-2:]
+        rows = self.fft_tiled_batched(img.reshape(-1, nx), cap, threads).reshape(img.shape)
+        cols = np.ascontiguousarray(np.swapaxes(rows, -1, -2))
+        del rows
+        out = self.fft_tiled_batched(cols.reshape(-1, ny), cap, threads).reshape(cols.shape)
+        return np.ascontiguousarray(np.swapaxes(out, -1, -2))
 
     def fft_levelwise(self, x, res=None):
         x = np.ascontiguousarray(x)
@@ -249,7 +287,15 @@ def available_reference() -> bool:
 
 
 def rel_l2(a: np.ndarray, b: np.ndarray) -> float:
-    a = a.astype(np.complex128).ravel()
-    b = b.astype(np.complex128).ravel()
-    den = np.linalg.norm(b)
-    return float(np.linalg.norm(a - b) / (den if den > 0 else 1.0))
+    a = np.asarray(a).ravel()
+    b = np.asarray(b).ravel()
+    assert a.shape == b.shape, (a.shape, b.shape)
+    num = den = 0.0
+    step = 1 << 24  # chunked: 2^30-point arrays would need 32 GB of complex128 temporaries
+    for s in range(0, a.size, step):
+        ac = a[s:s + step].astype(np.complex128)
+        bc = b[s:s + step].astype(np.complex128)
+        d = ac - bc
+        num += float(np.vdot(d, d).real)
+        den += float(np.vdot(bc, bc).real)
+    return float(np.sqrt(num) / (np.sqrt(den) if den > 0 else 1.0))

@@ -197,22 +197,6 @@ def test_stage_row_fft_and_interstage(tf, oracle):
     assert b.tile()[0, 0] == 1.0 and b.tile()[0, 1] == -1j
 
 
-@pytest.mark.parametrize("n", [1 << 16, 1 << 20, 1 << 24])
-def test_fast_mode_programmatic_launch_opt_in(tf, oracle, monkeypatch, n):
-    """TILEFFT_PDL=1: the plan's graph has programmatic kernel->kernel edges and
-    every pass waits (griddepcontrol.wait) for its predecessor: same output."""
-    x = oracle.random_bench_signal(n, 4).astype(np.complex64)
-    dp = tf._capi.DevicePlan.create(n, 1, None, 8, tf._capi.MODE_FAST, None, 0)
-    ref = np.empty_like(x)
-    dp.exec_host(x.ctypes.data, ref.ctypes.data, tf._capi.FORWARD)
-    monkeypatch.setenv("TILEFFT_PDL", "1")
-    dq = tf._capi.DevicePlan.create(n, 1, None, 8, tf._capi.MODE_FAST, None, 0)
-    for _ in range(3):
-        got = np.empty_like(x)
-        dq.exec_host(x.ctypes.data, got.ctypes.data, tf._capi.FORWARD)
-        assert bits_equal(got, ref)
-
-
 @pytest.mark.parametrize("n,b", [(2048, 300), (4096, 129), (8192, 64)])
 def test_fast_batched_long_rows_prefetch_kernel(tf, oracle, monkeypatch, n, b):
     """k_rows_pf (persistent long rows, next row streamed into the exchange region):
@@ -227,8 +211,38 @@ def test_fast_batched_long_rows_prefetch_kernel(tf, oracle, monkeypatch, n, b):
     xd = torch.from_numpy(x).cuda()
     dev = tf.fft_tiled_device(xd, tf.make_plan(n)).cpu().numpy()
     assert bits_equal(dev, got)
-    monkeypatch.setenv("TILEFFT_NO_ROWS_PF", "1")
-    tf.tilefft._plan_cache.clear()
-    ref = tf.fft_tiled(x, tf.make_plan(n))
-    tf.tilefft._plan_cache.clear()
-    assert bits_equal(ref, got)
+    # an 8-byte-aligned device buffer takes the non-persistent k_rows kernel: same bits
+    buf = torch.zeros(n * b + 1, dtype=torch.complex64, device="cuda")
+    buf[1:] = xd.reshape(-1)
+    unal = tf.fft_tiled_device(buf[1:].view(b, n), tf.make_plan(n)).cpu().numpy()
+    assert bits_equal(unal, got)
+
+
+@pytest.mark.parametrize("case", ["1d_2e22", "2d_4096x512"])
+def test_one_plan_two_streams_concurrently(tf, oracle, case):
+    """Execs of one plan on two streams share its workspace / two-level scratch
+    and counters: the plan orders them on the device, so launching both without
+    any host synchronisation gives bitwise the serial results."""
+    import torch
+    from paper_1707_07263_b200 import _capi
+    if case == "1d_2e22":
+        n = 1 << 22
+        dp = _capi.DevicePlan.create(n, 1, None, 8, _capi.MODE_FAST, None, 0)
+    else:
+        n = 4096 * 512
+        dp = _capi.DevicePlan.create_2d(4096, 512, 1, 8, 0)
+    xs = [torch.from_numpy(oracle.random_bench_signal(n, s).astype(np.complex64)).cuda() for s in (1, 2, 3, 4)]
+    serial = []
+    for x in xs:
+        y = torch.empty_like(x)
+        dp.exec_device(x.data_ptr(), y.data_ptr(), _capi.FORWARD, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        serial.append(y.cpu().numpy())
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for rep in range(3):
+        ys = [torch.empty_like(x) for x in xs]
+        for i, (x, y) in enumerate(zip(xs, ys)):
+            dp.exec_device(x.data_ptr(), y.data_ptr(), _capi.FORWARD, streams[i % 2].cuda_stream)
+        torch.cuda.synchronize()
+        for y, want in zip(ys, serial):
+            assert bits_equal(y.cpu().numpy(), want), rep

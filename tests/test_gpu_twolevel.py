@@ -98,12 +98,9 @@ def test_two_level_inverse_vs_oracle(tf, oracle):
     assert rel_l2(got, oracle.fft_tiled(x, inverse=True)) <= tol(n)
 
 
-@pytest.mark.parametrize("ws", ["1", "0"])
-def test_two_level_schedule_invariance(tf, oracle, monkeypatch, ws):
+def test_two_level_schedule_invariance(tf, oracle, monkeypatch):
     """Lag D and slot count only change which CTA runs which item and when:
-    the output is bit-identical (D=1 with 2 slots makes every dependency wait).
-    ws=1: the warp-specialised kernel (default), ws=0: the mixed-item kernel."""
-    monkeypatch.setenv("TILEFFT_TWO_WS", ws)
+    the output is bit-identical (D=1 with 2 slots makes every dependency wait)."""
     n = 1 << 24
     x = oracle.random_bench_signal(n, 3).astype(np.complex64)
     ref = _run(_plan(tf, n), x)
@@ -172,69 +169,3 @@ def test_two_level_2d_8192_square_roundtrip(tf, oracle):
         wy = np.exp(-2j * np.pi * (ky * np.arange(ny) % ny) / ny)
         exact = wy @ (x64 @ wx)  # separable direct sum, fp64
         assert abs(spec[ky, kx] - exact) <= 1e-5 * math.log2(ny * nx) * np.sqrt(e_x), (ky, kx)
-
-
-@pytest.mark.parametrize("logn", [16, 18, 21, 24])
-def test_warp_owned_comb_kernel_opt_in(tf, oracle, monkeypatch, logn):
-    """comb_w.cuh (TILEFFT_COMBW=1): warp-owned comb tiles, TMA in and out."""
-    monkeypatch.setenv("TILEFFT_COMBW", "1")
-    monkeypatch.delenv("TILEFFT_TWO_1D", raising=False)
-    n = 1 << logn
-    x = oracle.random_bench_signal(n, 2).astype(np.complex64)
-    got = _run(_plan(tf, n), x)
-    err = rel_l2(got, oracle.fft_tiled(x))
-    assert err <= tol(n) and err < 5e-7, err
-    inv = _run(_plan(tf, n), x, tf._capi.INVERSE)
-    assert rel_l2(inv, oracle.fft_tiled(x, inverse=True)) <= tol(n)
-
-
-@pytest.mark.parametrize("ny,nx", [(512, 512), (256, 1024), (4096, 128)])
-def test_warp_owned_comb_kernel_2d_opt_in(tf, oracle, monkeypatch, ny, nx):
-    monkeypatch.setenv("TILEFFT_COMBW", "1")
-    monkeypatch.setenv("TILEFFT_NO_TWO", "1")
-    img = oracle.random_bench_signal(ny * nx, 6).astype(np.complex64).reshape(ny, nx)
-    dp = tf._capi.DevicePlan.create_2d(ny, nx, 1, 8, 0)
-    out = np.empty_like(img)
-    dp.exec_host(img.ctypes.data, out.ctypes.data, tf._capi.FORWARD)
-    assert rel_l2(out, oracle.fft2(img)) <= tol(ny * nx)
-
-
-@pytest.mark.parametrize("case", ["1d", "2d"])
-def test_two_level_warp_specialised_matches_mixed_kernel(tf, oracle, monkeypatch, case):
-    """k_two_ws (A team / B team, W_L^{n1 k2} applied by the B team) vs k_two
-    (one item queue, root applied by the A item): same transform."""
-    def run():
-        if case == "1d":
-            n = 1 << 23
-            x = oracle.random_bench_signal(n, 8).astype(np.complex64)
-            return _run(_plan(tf, n), x), oracle.fft_tiled(x), n
-        img = oracle.random_bench_signal(4096 * 512, 8).astype(np.complex64).reshape(4096, 512)
-        dp = tf._capi.DevicePlan.create_2d(4096, 512, 1, 8, 0)
-        out = np.empty_like(img)
-        dp.exec_host(img.ctypes.data, out.ctypes.data, tf._capi.FORWARD)
-        return out, oracle.fft2(img), img.size
-    a, want, n = run()
-    monkeypatch.setenv("TILEFFT_TWO_WS", "0")
-    b, _, _ = run()
-    assert rel_l2(a, want) <= tol(n) and rel_l2(b, want) <= tol(n)
-    assert rel_l2(a, b) < 1e-6
-
-
-@pytest.mark.parametrize("logn", [14, 15, 18, 19, 20])
-def test_fused_small_two_pass_opt_in(tf, oracle, monkeypatch, logn):
-    """K_SMALL2 (TILEFFT_FUSE=1): both passes of a small plan in one launch with
-    a dynamic tile counter; repeated executions exercise the monotonic counters."""
-    monkeypatch.setenv("TILEFFT_FUSE", "1")
-    monkeypatch.delenv("TILEFFT_TWO_1D", raising=False)
-    n = 1 << logn
-    dp = _plan(tf, n)
-    info = dp.info()
-    assert info["launches_per_exec"] == 1 and info["passes"] == 2
-    x = oracle.random_bench_signal(n, 9).astype(np.complex64)
-    want = oracle.fft_tiled(x)
-    first = _run(dp, x)
-    assert rel_l2(first, want) <= tol(n) and rel_l2(first, want) < 5e-7
-    for _ in range(3):
-        assert bits_equal(_run(dp, x), first)
-    inv = _run(dp, x, tf._capi.INVERSE)
-    assert rel_l2(inv, oracle.fft_tiled(x, inverse=True)) <= tol(n)
