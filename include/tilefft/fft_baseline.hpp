@@ -10,6 +10,7 @@
 #include <utility>
 #include <vector>
 
+#include "tilefft/access_patterns.hpp"
 #include "tilefft/b200_runtime.hpp"
 #include "tilefft/common.hpp"
 #include "tilefft/exec_model.hpp"
@@ -56,17 +57,20 @@ Signal<Real> run_levelwise(const Signal<Real>& x, const TwiddleTable<Real>& tabl
 template <typename Real>
 Signal<Real> fft_levelwise(const Signal<Real>& x, const TwiddleTable<Real>& table, AccessRecorder* trace = nullptr) {
   Signal<Real> out = detail::run_levelwise(x, table, TILEFFT_FORWARD);
-  if (trace != nullptr) {  // fft_baseline.hpp:80-113 counters
+  if (trace != nullptr) {  // fft_baseline.hpp:80-113: the reorder sweep, then one stage per level
     const std::uint64_t n = x.size();
+    const auto slow = [&](std::span<const std::uint64_t> a, bool) { trace->record_slow_request(a); };
     trace->begin_reorder();
     trace->add_slow_reads(n);
     trace->add_slow_writes(n);
+    detail::for_each_reorder_request(n, trace->config(), slow);
     trace->add_barrier();
-    for (unsigned l = 0; l < log2_exact(n); ++l) {
+    for (unsigned lv = 1; lv <= log2_exact(n); ++lv) {
       trace->begin_stage();
       trace->add_slow_reads(n);
       trace->add_slow_writes(n);
       trace->add_twiddle_fetches(n / 2);
+      detail::for_each_levelwise_request(n, lv, trace->config(), slow);
       trace->add_barrier();
     }
   }

@@ -17,6 +17,7 @@
 #include <utility>
 #include <vector>
 
+#include "tilefft/access_patterns.hpp"
 #include "tilefft/b200_runtime.hpp"
 #include "tilefft/common.hpp"
 #include "tilefft/exec_model.hpp"
@@ -71,19 +72,26 @@ void unpack_rows(FastBuffer<Real>& buf, const std::vector<Complex<Real>>& t) {
     for (std::size_t c = 0; c < buf.cols(); ++c) buf.at(r, c) = t[r * buf.cols() + c];
 }
 
-// Per-pass counters fft_tiled records (tiled_fft.hpp:382-401): every pass
-// reads and writes all n elements once; fast accesses are the tile load,
-// 2 per element per level, and the store; twiddle fetches are L-1 per tile
-// plus one per element on inner passes.
+// The per-pass trace fft_tiled records (tiled_fft.hpp:382-402): every pass
+// reads and writes all n elements once, in-tile accesses and root fetches per
+// the pass's tile shape, the gather and scatter sweeps' warp requests
+// (coalesced into segments) and the tile's half-warp column streams (bank
+// conflicts), one barrier. The GPU executes exactly these passes' element
+// movement; the request shapes are the reference's model of them.
 inline void record_trace(const StagePlan& plan, AccessRecorder& trace) {
+  const auto slow = [&](std::span<const std::uint64_t> a, bool) { trace.record_slow_request(a); };
   for (std::size_t s = 1; s <= plan.pass_count(); ++s) {
     const StageGeometry& g = plan.stage(s);
-    const std::uint64_t n = plan.n_total;
+    const std::uint64_t n = plan.n_total, occasions = column_stream_occasions(plan, s);
     trace.begin_stage();
     trace.add_slow_reads(n);
     trace.add_slow_writes(n);
-    trace.add_fast_accesses(n + 2 * n * g.levels + n);
-    trace.add_twiddle_fetches(g.tile_count * (g.fft_len - 1) + (s < plan.pass_count() ? n : 0));
+    trace.add_fast_accesses(n * occasions);
+    trace.add_twiddle_fetches(stage_twiddle_fetches(plan, s));
+    for_each_tiled_sweep_request(plan, s, /*gather=*/true, trace.config(), slow);
+    for_each_tiled_sweep_request(plan, s, /*gather=*/false, trace.config(), slow);
+    for_each_column_stream(g.rows, g.fft_len, g.padded_stride, trace.config(),
+                           [&](std::span<const std::uint64_t> w) { trace.record_fast_request_repeated(w, occasions); });
     trace.add_barrier();
   }
 }
@@ -150,6 +158,8 @@ Signal<Real> exchange_transpose(const Signal<Real>& data, std::size_t stage, con
     trace->begin_stage();
     trace->add_slow_reads(data.size());
     trace->add_slow_writes(data.size());
+    detail::for_each_exchange_request(plan, stage, trace->config(),
+                                      [&](std::span<const std::uint64_t> a, bool) { trace->record_slow_request(a); });
     trace->add_barrier();
   }
   return out;

@@ -146,6 +146,16 @@ TILEFFT_API int tilefft_ipc_close_handle(void* dptr);
  * (build_twiddle_table, twiddle.hpp:47-73; bit-identical values). */
 TILEFFT_API int tilefft_build_twiddle(uint64_t resolution, uint32_t elem_bytes, void* out);
 
+/* The reference's cost model (memsim.hpp:38-95, access_patterns.hpp): the
+ * closed-form AccessStats of fft_tiled under make_plan(n, tile_capacity)
+ * (algorithm TILEFFT_ACCOUNT_TILED) or of fft_levelwise (…_LEVELWISE), as
+ * stats[7] = {slow_elem_reads, slow_elem_writes, slow_transactions,
+ * fast_accesses, bank_conflict_cycles, barriers, twiddle_fetches}. Host only;
+ * the C++ drop-in records the same figures in traced calls. */
+#define TILEFFT_ACCOUNT_TILED 0
+#define TILEFFT_ACCOUNT_LEVELWISE 1
+TILEFFT_API int tilefft_account(uint64_t n, uint64_t tile_capacity, uint32_t algorithm, uint64_t* stats);
+
 /* Thread-local message of the last failing call ("" if none). */
 TILEFFT_API const char* tilefft_last_error(void);
 

@@ -16,6 +16,7 @@
 
 #include "tilefft/bench.hpp"
 #include "tilefft/fft_baseline.hpp"
+#include "tilefft/memsim.hpp"
 #include "tilefft/reference_dft.hpp"
 #include "tilefft/stage_plan.hpp"
 #include "tilefft/tiled_fft.hpp"
@@ -164,4 +165,24 @@ int ref_ctx_exec_batched(void* vc, const float* x, float* out, uint64_t batch, u
 }
 
 uint32_t ref_hardware_concurrency() { return std::thread::hardware_concurrency(); }
+
+// memsim.hpp:58-95 / :38-55: the reference's closed-form accounting, seven
+// counters in AccessStats order (cost-model parity, tests/test_costmodel.py).
+static void put_stats(const tilefft::AccessStats& s, uint64_t* out) {
+  const uint64_t v[7] = {s.slow_elem_reads, s.slow_elem_writes, s.slow_transactions, s.fast_accesses,
+                         s.bank_conflict_cycles, s.barriers, s.twiddle_fetches};
+  std::memcpy(out, v, sizeof v);
+}
+int ref_account_tiled(uint64_t n, uint64_t cap, uint64_t* out) {
+  try {
+    put_stats(tilefft::account_tiled(tilefft::make_plan(n, cap)), out);
+    return 0;
+  } catch (const std::invalid_argument&) { return -1; }
+}
+int ref_account_levelwise(uint64_t n, uint64_t* out) {
+  try {
+    put_stats(tilefft::account_levelwise(n), out);
+    return 0;
+  } catch (const std::invalid_argument&) { return -1; }
+}
 }

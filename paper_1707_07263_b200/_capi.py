@@ -55,6 +55,7 @@ EXPORTS = (
     "tilefft_plan_destroy",
     "tilefft_plan_info",
     "tilefft_build_twiddle",
+    "tilefft_account",
     "tilefft_exchange",
     "tilefft_interstage_scale",
     "tilefft_dist_plan_create",
@@ -100,6 +101,7 @@ def load() -> ctypes.CDLL:
         lib.tilefft_plan_destroy.argtypes = [vp]
         lib.tilefft_plan_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
         lib.tilefft_build_twiddle.argtypes = [u64, u32, vp]
+        lib.tilefft_account.argtypes = [u64, u64, u32, ctypes.POINTER(u64)]
         lib.tilefft_exchange.argtypes = [vp, vp, u64, ctypes.POINTER(u64), u32, u32, u32, i32]
         lib.tilefft_interstage_scale.argtypes = [vp, vp, u64, u64, u64, u64, u64, vp, u64, u32, i32]
         lib.tilefft_dist_plan_create.argtypes = [ctypes.POINTER(vp), u64, u32, u32, u32, i32]
@@ -113,7 +115,8 @@ def load() -> ctypes.CDLL:
         lib.tilefft_last_error.restype = ctypes.c_char_p
         lib.tilefft_version.restype = ctypes.c_char_p
         for name in ("tilefft_plan_create", "tilefft_plan_create_2d", "tilefft_exec_c2c", "tilefft_exec_c2c_host",
-                     "tilefft_plan_destroy", "tilefft_plan_info", "tilefft_build_twiddle", "tilefft_exchange",
+                     "tilefft_plan_destroy", "tilefft_plan_info", "tilefft_build_twiddle", "tilefft_account",
+                     "tilefft_exchange",
                      "tilefft_interstage_scale", "tilefft_dist_plan_create", "tilefft_dist_layout",
                      "tilefft_dist_set_peers", "tilefft_dist_exec_pass1", "tilefft_dist_exec_pass2",
                      "tilefft_ipc_get_handle", "tilefft_ipc_open_handle", "tilefft_ipc_close_handle"):
@@ -199,6 +202,19 @@ def interstage_scale(h_in: int, h_out: int, rows: int, cols: int, row0: int, row
     check(load().tilefft_interstage_scale(ctypes.c_void_p(h_in), ctypes.c_void_p(h_out), int(rows), int(cols),
                                           int(row0), int(rows_per_sub), int(sub_len), ctypes.c_void_p(table_ptr),
                                           int(resolution), int(elem_bytes), int(device)))
+
+
+ACCOUNT_TILED = 0
+ACCOUNT_LEVELWISE = 1
+ACCESS_STATS_FIELDS = ("slow_elem_reads", "slow_elem_writes", "slow_transactions", "fast_accesses",
+                       "bank_conflict_cycles", "barriers", "twiddle_fetches")
+
+
+def account(n: int, tile_capacity: int, algorithm: int) -> dict:
+    """The reference's cost model (memsim.hpp) through tilefft_account: host only."""
+    out = (ctypes.c_uint64 * 7)()
+    check(load().tilefft_account(int(n), int(tile_capacity), int(algorithm), out))
+    return dict(zip(ACCESS_STATS_FIELDS, (int(v) for v in out)))
 
 
 def build_twiddle(resolution: int, elem_bytes: int, out_ptr: int) -> None:

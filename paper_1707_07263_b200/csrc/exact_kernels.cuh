@@ -38,7 +38,7 @@ template <typename Real>
 __global__ void k_exact_pass(const C2<Real>* in, C2<Real>* out, ExactArgs a, const C2<Real>* __restrict__ tbl,
                              Real scale) {
   using V = C2<Real>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   V* row = reinterpret_cast<V*>(smem_raw);
   const long long id = blockIdx.x;
   const long long batch = id / a.rows, grow = id % a.rows;

@@ -237,7 +237,7 @@ k_rows(const C2<Real>* in, C2<Real>* out, long long nrows, const C2<Real>* __res
   using Cfg = RowsCfg<Real, L, FPC>;
   using V = C2<Real>;
   using Sh = typename Cfg::Sh;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   V* sm = reinterpret_cast<V*>(smem_raw);
   const int ff = threadIdx.x / Sh::T, t = threadIdx.x % Sh::T;
   long long row = (long long)blockIdx.x * FPC + ff;
@@ -504,7 +504,7 @@ template <typename Real, int L, bool INV, bool TWID, int MODE, int F_ = FOf<Real
 __global__ void __launch_bounds__(CombCfg<Real, L, F_>::THREADS, CombCfg<Real, L, F_>::MINB)
 k_comb(const C2<Real>* in, C2<Real>* out, CombArgs a, const C2<Real>* __restrict__ tw,
        const double2* __restrict__ wc, const double2* __restrict__ wf, Real scale) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   comb_tile<Real, L, INV, TWID, MODE, F_>(in, out, a, tw, wc, wf, scale, blockIdx.x,
                                           reinterpret_cast<C2<Real>*>(smem_raw));
 }
@@ -770,7 +770,7 @@ __device__ __forceinline__ void final_tile(const C2<Real>* in, C2<Real>* out, co
 template <typename Real, int L, bool INV, int F_ = FOf<Real>::v>
 __global__ void __launch_bounds__(FinalCfg<Real, L, F_>::THREADS, FinalCfg<Real, L, F_>::THREADS <= 256 ? 2 : 1)
 k_final_t(const C2<Real>* in, C2<Real>* out, FinalArgs a, const C2<Real>* __restrict__ tw, Real scale) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   final_tile<Real, L, INV, F_>(in, out, a, tw, scale, blockIdx.x, reinterpret_cast<C2<Real>*>(smem_raw));
 }
 

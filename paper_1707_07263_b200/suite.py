@@ -19,9 +19,12 @@ reference caps at 2^20, bench.hpp:173-177); ``wall_time_ns`` is the
 reference's best-of-R host-to-host time (vector in, vector out) and
 ``device_time_ns`` the best-of-R device-resident time (CUDA events);
 ``slow_elem_accesses`` / ``barriers`` follow the reference's 2 N p law for the
-device passes actually run (memsim.hpp:59-63); the simulated-Fermi counters
-``slow_transactions`` / ``bank_conflict_cycles`` are not modelled (SURVEY §2
-rows 7-9: out of scope) and are reported as 0. The reference's CSV writer
+device passes actually run (memsim.hpp:59-63). ``slow_transactions`` /
+``bank_conflict_cycles`` are the reference's cost model (memsim.hpp, through
+``tilefft_account``) for the rows that execute the reference's algorithm
+(``levelwise``, ``tiled``); the model does not describe the fast tier's
+radix-32 kernels or cuFFT, so those rows carry -1 ("not modelled"), never a
+misleading 0. The reference's CSV writer
 prints the algorithm name twice (bench.hpp:303-304); this one prints it once.
 """
 from __future__ import annotations
@@ -198,7 +201,9 @@ def run_suite(sizes: List[int], options: SuiteOptions = SuiteOptions()) -> List[
             wall = _best_ns(options.repetitions, lambda: tf.fft_levelwise(x, table))
             dev_ns = _device_best_ns(options.repetitions, lambda: lw.exec_device(xd.data_ptr(), yd.data_ptr(),
                                                                                    _capi.FORWARD, stream()))
-            push(BenchRow(n, "levelwise", levels, check("levelwise", y), 2 * n * levels, 0, 0, levels, wall,
+            lwm = _capi.account(n, options.tile_capacity, _capi.ACCOUNT_LEVELWISE)
+            push(BenchRow(n, "levelwise", levels, check("levelwise", y), 2 * n * levels, lwm["slow_transactions"],
+                          lwm["bank_conflict_cycles"], levels, wall,
                           options.repetitions, dev_ns, flops / dev_ns, 2 * n * (levels + 1) * dt.itemsize / dev_ns))
 
             # tiled (exact tier): the reference's own plan and table, bit for bit
@@ -208,7 +213,9 @@ def run_suite(sizes: List[int], options: SuiteOptions = SuiteOptions()) -> List[
             wall = _best_ns(options.repetitions, lambda: tf.fft_tiled(x, plan, table, mode="exact"))
             dev_ns = _device_best_ns(options.repetitions, lambda: ex.exec_device(xd.data_ptr(), yd.data_ptr(),
                                                                                    _capi.FORWARD, stream()))
-            push(BenchRow(n, "tiled", p, check("tiled", y), 2 * n * p, 0, 0, p, wall, options.repetitions, dev_ns,
+            tm = _capi.account(n, options.tile_capacity, _capi.ACCOUNT_TILED)
+            push(BenchRow(n, "tiled", p, check("tiled", y), 2 * n * p, tm["slow_transactions"],
+                          tm["bank_conflict_cycles"], p, wall, options.repetitions, dev_ns,
                           flops / dev_ns, 2 * n * p * dt.itemsize / dev_ns))
 
         # b200 (fast tier, the product path)
@@ -218,14 +225,14 @@ def run_suite(sizes: List[int], options: SuiteOptions = SuiteOptions()) -> List[
         wall = _best_ns(options.repetitions, lambda: tf.fft_tiled(x, plan))
         dev_ns = _device_best_ns(options.repetitions, lambda: fp.exec_device(xd.data_ptr(), yd.data_ptr(),
                                                                                _capi.FORWARD, stream()))
-        push(BenchRow(n, "b200", dp, check("b200", y), 2 * n * dp, 0, 0, dp, wall, options.repetitions, dev_ns,
+        push(BenchRow(n, "b200", dp, check("b200", y), 2 * n * dp, -1, -1, dp, wall, options.repetitions, dev_ns,
                       flops / dev_ns, 2 * n * dp * dt.itemsize / dev_ns))
 
         if options.include_cufft:
             y = torch.fft.fft(xd).cpu().numpy()
             wall = _best_ns(options.repetitions, lambda: torch.fft.fft(torch.from_numpy(x).to(dev)).cpu())
             dev_ns = _device_best_ns(options.repetitions, lambda: torch.fft.fft(xd))
-            push(BenchRow(n, "cufft", 0, check("cufft", y), 0, 0, 0, 0, wall, options.repetitions, dev_ns,
+            push(BenchRow(n, "cufft", 0, check("cufft", y), 0, -1, -1, 0, wall, options.repetitions, dev_ns,
                           flops / dev_ns, 0.0))
         del xd, yd
     return rows

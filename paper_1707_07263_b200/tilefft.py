@@ -182,6 +182,27 @@ def twiddle_lookup(table: TwiddleTable, n: int, e: int):  # twiddle.hpp:79-91
     return table.values[(e % n) * (table.resolution // n)]
 
 
+# ---- cost model (memsim.hpp / access_patterns.hpp, host logic) -------------------------------------
+def account_tiled(plan: StagePlan) -> dict:
+    """memsim.hpp:58-95: the reference's closed-form AccessStats of fft_tiled under `plan`."""
+    _require(plan.pass_count() >= 1, "account_tiled: empty plan")
+    _require(plan.bank_count == ExecConfig().bank_count, "account_tiled: plan was built for a different bank count")
+    return _capi.account(plan.n_total, plan.tile_capacity, _capi.ACCOUNT_TILED)
+
+
+def account_levelwise(n: int) -> dict:
+    """memsim.hpp:38-55: AccessStats of fft_levelwise (the reorder sweep excluded)."""
+    _require(is_power_of_two(n) and n >= 2, "account_levelwise: n must be a power of two >= 2")
+    return _capi.account(n, 2, _capi.ACCOUNT_LEVELWISE)
+
+
+def reduction_ratio(n: int, plan: StagePlan) -> float:
+    """memsim.hpp:99-104."""
+    _require(n == plan.n_total, "reduction_ratio: n does not match the plan")
+    _require(plan.pass_count() >= 1, "reduction_ratio: empty plan")
+    return log2_exact(n) / plan.pass_count()
+
+
 # ---- execution ------------------------------------------------------------------------------------
 _plan_cache: dict = {}
 _cache_lock = threading.Lock()

@@ -311,6 +311,37 @@ int main() {
     CHECK(w < 1e-3);
   });
 
+  run("criteria 4 and 7: traced GPU runs equal the closed-form accounting (acceptance_main.cpp:158-195)", [] {
+    const auto table = build_twiddle_table<double>(65536);
+    const std::size_t cases[][2] = {{2, 1024},     {16, 4},      {16, 1024},  {256, 16},   {256, 1024},
+                                    {4096, 64},    {4096, 1024}, {16384, 1024}, {65536, 1024}};
+    for (const auto& c : cases) {
+      const auto x = random_signal(c[0], 0x4A55 + c[0]);
+      AccessRecorder lt;
+      (void)fft_levelwise(x, table, &lt);
+      const unsigned bits = log2_exact(c[0]);
+      CHECK(lt.totals() == account_levelwise(c[0]));
+      CHECK(lt.totals().slow_elem_accesses() == 2 * c[0] * bits && lt.totals().barriers == bits);
+      CHECK(lt.reorder().slow_transactions > 0 && lt.reorder().barriers == 1);
+      const StagePlan plan = make_plan(c[0], c[1]);
+      AccessRecorder tt;
+      (void)fft_tiled(x, plan, table, &tt);
+      CHECK(tt.totals() == account_tiled(plan));
+      CHECK(tt.stage_count() == plan.pass_count() && tt.totals().barriers == plan.pass_count());
+      CHECK(tt.totals().slow_elem_accesses() == 2 * c[0] * plan.pass_count());
+      CHECK(tt.totals().slow_transactions > 0);
+    }
+    CHECK(reduction_ratio(4096, make_plan(4096)) == 6.0 && reduction_ratio(65536, make_plan(65536)) == 8.0);
+  });
+
+  run("exchange_transpose records one full sweep (test_tiled_fft.cpp:187-198)", [] {
+    AccessRecorder trace;
+    (void)exchange_transpose(random_signal(256, 32), 1, make_plan(256, 16), &trace);
+    CHECK(trace.stage_count() == 1);
+    CHECK(trace.stage(1).slow_elem_reads == 256 && trace.stage(1).slow_elem_writes == 256);
+    CHECK(trace.stage(1).barriers == 1 && trace.stage(1).slow_transactions > 0);
+  });
+
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail;
 }

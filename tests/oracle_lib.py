@@ -193,6 +193,8 @@ class Reference:
         L.ref_ctx_exec_single.argtypes = [vp, vp, vp, u32]
         L.ref_ctx_exec_batched.argtypes = [vp, vp, vp, u64, u32]
         L.ref_hardware_concurrency.restype = u32
+        L.ref_account_tiled.argtypes = [u64, u64, vp]
+        L.ref_account_levelwise.argtypes = [u64, vp]
 
     def fft_tiled(self, x, cap=1024, res=None, threads=1, inverse=False):
         x = np.ascontiguousarray(x)
@@ -234,6 +236,19 @@ class Reference:
         del rows
         out = self.fft_tiled_batched(cols.reshape(-1, ny), cap, threads).reshape(cols.shape)
         return np.ascontiguousarray(np.swapaxes(out, -1, -2))
+
+    def account_tiled(self, n, cap=1024):
+        """memsim.hpp account_tiled(make_plan(n, cap)): 7 counters in AccessStats order."""
+        out = np.zeros(7, np.uint64)
+        if self.lib.ref_account_tiled(n, cap, _ptr(out)) != 0:
+            raise ValueError("account_tiled: invalid argument")
+        return [int(v) for v in out]
+
+    def account_levelwise(self, n):
+        out = np.zeros(7, np.uint64)
+        if self.lib.ref_account_levelwise(n, _ptr(out)) != 0:
+            raise ValueError("account_levelwise: invalid argument")
+        return [int(v) for v in out]
 
     def fft_levelwise(self, x, res=None):
         x = np.ascontiguousarray(x)
