@@ -46,10 +46,10 @@ Signal<Real> run_levelwise(const Signal<Real>& x, const TwiddleTable<Real>& tabl
   detail::require(is_power_of_two(n) && n >= 2, "fft_levelwise: signal length must be a power of two >= 2");
   detail::require(table.resolution >= n && table.resolution % n == 0,
                   "fft_levelwise: signal length must divide the table resolution");
-  tilefft_plan_t p = runtime::device_plan(n, 1, {}, sizeof(Complex<Real>), TILEFFT_MODE_LEVELWISE,
+  const auto p = runtime::device_plan(n, 1, {}, sizeof(Complex<Real>), TILEFFT_MODE_LEVELWISE,
                                           table.values.data(), table.resolution);
   Signal<Real> out(n);
-  runtime::check(tilefft_exec_c2c_host(p, x.data(), out.data(), sign));
+  runtime::check(tilefft_exec_c2c_host(p.get(), x.data(), out.data(), sign));
   return out;
 }
 }  // namespace detail

@@ -100,11 +100,11 @@ template <typename Real>
 Signal<Real> run_tiled(const Signal<Real>& x, const StagePlan& plan, const TwiddleTable<Real>& table, int sign) {
   const ExecMode mode = exec_mode();
   const std::vector<std::uint64_t> f(plan.factors.begin(), plan.factors.end());
-  tilefft_plan_t p = runtime::device_plan(plan.n_total, 1, f, sizeof(Complex<Real>), static_cast<unsigned>(mode),
+  const auto p = runtime::device_plan(plan.n_total, 1, f, sizeof(Complex<Real>), static_cast<unsigned>(mode),
                                           mode == ExecMode::exact ? static_cast<const void*>(table.values.data()) : nullptr,
                                           mode == ExecMode::exact ? table.resolution : 0);
   Signal<Real> out(x.size());
-  runtime::check(tilefft_exec_c2c_host(p, x.data(), out.data(), sign));
+  runtime::check(tilefft_exec_c2c_host(p.get(), x.data(), out.data(), sign));
   return out;
 }
 
@@ -119,9 +119,9 @@ void stage_row_fft(FastBuffer<Real>& buf, std::size_t length, const TwiddleTable
                   "stage_row_fft: length must divide the table resolution");
   if (length < 2) return;
   std::vector<Complex<Real>> t = detail::pack_rows(buf);
-  tilefft_plan_t p = runtime::device_plan(length, buf.rows(), {length}, sizeof(Complex<Real>), TILEFFT_MODE_EXACT,
+  const auto p = runtime::device_plan(length, buf.rows(), {length}, sizeof(Complex<Real>), TILEFFT_MODE_EXACT,
                                           table.values.data(), table.resolution);
-  runtime::check(tilefft_exec_c2c_host(p, t.data(), t.data(), TILEFFT_FORWARD));
+  runtime::check(tilefft_exec_c2c_host(p.get(), t.data(), t.data(), TILEFFT_FORWARD));
   detail::unpack_rows(buf, t);
 }
 

@@ -14,7 +14,10 @@ Complex data is numpy ``complex64`` (Real=float) or ``complex128``
 """
 from __future__ import annotations
 
+import collections
 import dataclasses
+import hashlib
+import os
 import threading
 from typing import List, Optional
 
@@ -204,20 +207,37 @@ def reduction_ratio(n: int, plan: StagePlan) -> float:
 
 
 # ---- execution ------------------------------------------------------------------------------------
-_plan_cache: dict = {}
+_plan_cache: "collections.OrderedDict" = collections.OrderedDict()
 _cache_lock = threading.Lock()
+# Each cached plan pins device workspace and host staging: least recently
+# used plans are released beyond this many entries.
+PLAN_CACHE_CAPACITY = int(os.environ.get("TILEFFT_PLAN_CACHE", "16"))
+
+
+def _cached_plan(key, create):
+    with _cache_lock:
+        p = _plan_cache.get(key)
+        if p is None:
+            p = create()
+            _plan_cache[key] = p
+            while len(_plan_cache) > max(1, PLAN_CACHE_CAPACITY):
+                _plan_cache.popitem(last=False)  # released when its last user drops it (DevicePlan.__del__)
+        else:
+            _plan_cache.move_to_end(key)
+        return p
 
 
 def _device_plan(n, batch, factors, elem_bytes, mode, table, device):
     uses_table = table is not None and mode in (_capi.MODE_EXACT, _capi.MODE_LEVELWISE)
-    key = (n, batch, tuple(factors) if factors else None, elem_bytes, mode,
-           (table.resolution, table.values.ctypes.data) if uses_table else None, device)
-    with _cache_lock:
-        p = _plan_cache.get(key)
-        if p is None:
-            p = _capi.DevicePlan.create(n, batch, factors, elem_bytes, mode, table if uses_table else None, device)
-            _plan_cache[key] = p
-        return p
+    # FAST plans choose their own device passes: keyed by shape only. Table
+    # plans copy the roots they use at creation: keyed by those roots' bytes.
+    fp = None
+    if uses_table:
+        roots = table.values[:: table.resolution // n][:n]
+        fp = (table.resolution, hashlib.blake2b(np.ascontiguousarray(roots).tobytes(), digest_size=16).hexdigest())
+    key = (n, batch, tuple(factors) if (factors and mode != _capi.MODE_FAST) else None, elem_bytes, mode, fp, device)
+    return _cached_plan(key, lambda: _capi.DevicePlan.create(n, batch, factors, elem_bytes, mode,
+                                                             table if uses_table else None, device))
 
 
 _MODES = {"fast": _capi.MODE_FAST, "exact": _capi.MODE_EXACT, "permute": _capi.MODE_PERMUTE}
@@ -385,11 +405,7 @@ def fft2_tiled(x, device: int = 0, inverse: bool = False) -> np.ndarray:
     ny, nx = x.shape[-2:]
     batch = int(np.prod(x.shape[:-2])) if x.ndim > 2 else 1
     key = ("2d", ny, nx, batch, x.dtype.itemsize, device)
-    with _cache_lock:
-        dp = _plan_cache.get(key)
-        if dp is None:
-            dp = _capi.DevicePlan.create_2d(ny, nx, batch, x.dtype.itemsize, device)
-            _plan_cache[key] = dp
+    dp = _cached_plan(key, lambda: _capi.DevicePlan.create_2d(ny, nx, batch, x.dtype.itemsize, device))
     out = np.empty_like(x)
     dp.exec_host(x.ctypes.data, out.ctypes.data, _capi.INVERSE if inverse else _capi.FORWARD)
     return out
