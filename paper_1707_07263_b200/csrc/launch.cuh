@@ -298,6 +298,31 @@ int launch_two_k(const Pass& ps, const void* in, void* out, const void* tb, cons
     return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled failed for the two-level pass");
   const float2* t = (const float2*)tb;
   const double2* t64 = (const double2*)tb64;
+  if (ps.two_kernel != 0) {
+    // barrier-free TMA kernel (default): input tiles 128-byte swizzled, scratch read back by TMA
+    CUtensorMap tin, tscr;
+    if (enc(&tin, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(in), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled failed for the two-level pass");
+    const cuuint64_t sdims[4] = {(cuuint64_t)LA, 16, (cuuint64_t)LB, (cuuint64_t)a.nslot};
+    const cuuint64_t sstr[3] = {(cuuint64_t)LA * 8, (cuuint64_t)LA * 8 * 16, (cuuint64_t)LA * 8 * 16 * LB};
+    const cuuint32_t sbox[4] = {16, 16, (cuuint32_t)LB, 1};
+    if (enc(&tscr, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, a.scratch, sdims, sstr, sbox, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled failed for the two-level scratch");
+    auto launch = [&](auto kfn, int threads, int smem) -> int {
+      if (int rc = ensure_smem((const void*)kfn, smem)) return rc;
+      CUDA_TRY(cudaMemsetAsync(a.ctrl, 0, sizeof(unsigned) * (2 + 2 * a.nslot), st));
+      kfn<<<sm_count(), threads, smem, st>>>(tin, tscr, (float2*)out, a, t + ps.tw_off, t + ps.twl_off,
+                                             t64 + ps.wc_off, t64 + ps.wf_off, scale);
+      CUDA_TRY(cudaGetLastError());
+      return 0;
+    };
+    using TC = tfb::TwoTmaCfg<LA, LB>;
+    return launch(tfb::k_two_tma<LA, LB, INV, OUTT, TWID>, TC::THREADS, TC::SMEM);
+  }
   // warp-specialised two-level kernel: one 512-thread CTA per SM (A team + B team)
   using WCfg = tfb::TwoWsCfg<LA, LB, INV, OUTT>;
   auto kw = tfb::k_two_ws<LA, LB, INV, OUTT, TWID>;

@@ -266,6 +266,9 @@ std::vector<uint64_t> balanced_factors(uint64_t n, uint64_t cap) {
 
 
 // ---------------------------------------------------------------- two-level passes
+// diagnostics: the last two-level pass created with TILEFFT_TWO_TRACE set
+unsigned long long* g_two_trace = nullptr;
+size_t g_two_trace_bytes = 0;
 bool env_flag(const char* name) {
   const char* e = std::getenv(name);
   return e && *e && *e != '0';
@@ -314,6 +317,19 @@ Pass make_two_pass(tilefft_plan_s* P, TableBuilder<Real>& tb, uint64_t L, long l
   if (a.D > a.groups) a.D = (int)a.groups;
   a.nslot = std::max(a.D + 1, env_int("TILEFFT_TWO_NSLOT", 2 * a.D));
   a.discard = env_int("TILEFFT_TWO_DISCARD", 1);
+  ps.two_kernel = env_int("TILEFFT_TWO_KERNEL", 1);
+  a.diag = env_int("TILEFFT_TWO_DIAG", 0);
+  a.trace = nullptr;
+  if (env_flag("TILEFFT_TWO_TRACE")) {  // diagnostics: per-item timestamps, read by tilefft_debug_two_trace
+    const size_t bytes = (size_t)a.groups * ps.lb * 2 * 8 * sizeof(unsigned long long);
+    if (cudaMalloc(&a.trace, bytes) == cudaSuccess) {
+      cudaMemset(a.trace, 0, bytes);
+      g_two_trace = a.trace;
+      g_two_trace_bytes = bytes;
+    } else {
+      a.trace = nullptr;
+    }
+  }
   ps.two_cols = cols;
   ps.two_es_in = es_in;
   return ps;
@@ -671,6 +687,18 @@ int with_device_buffers(int device, const void* h_in, void* h_out, size_t in_byt
 }  // namespace
 
 // ================================================================ C ABI
+// Diagnostics only (not part of include/tilefft_b200.h): copy the per-item timestamps of the
+// last traced two-level pass (TILEFFT_TWO_TRACE=1) to host memory; returns the bytes available.
+extern "C" TILEFFT_API long long tilefft_debug_two_trace(void* host, long long bytes) {
+  if (!g_two_trace) return 0;
+  if (host && bytes > 0) {
+    cudaDeviceSynchronize();
+    cudaMemcpy(host, g_two_trace, std::min((size_t)bytes, g_two_trace_bytes),
+               cudaMemcpyDeviceToHost);
+  }
+  return (long long)g_two_trace_bytes;
+}
+
 extern "C" {
 
 const char* tilefft_last_error(void) { return g_err.c_str(); }

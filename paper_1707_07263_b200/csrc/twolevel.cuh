@@ -37,11 +37,19 @@ struct TwoArgs {
   int D;                     // lag between A(g) and B(g) in the hand-out order (groups)
   int nslot;                 // scratch slots (> D)
   int discard;               // discard consumed scratch lines from L2
+  int diag;                  // K_TWO_TMA diagnostics: 1 = data movement only (no FFT arithmetic)
   int fb;                    // fine-table bits of the inter-pass root tables
   uint32_t m_mask;           // M - 1 (inter-pass root W_M)
   float2* scratch;           // nslot * L * 16 elements
   unsigned* ctrl;            // [0] work counter, [1..nslot] A done, [nslot+1..2 nslot] B done
+  unsigned long long* trace; // diagnostics (TILEFFT_TWO_TRACE): 8 timestamps per item id, else null
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <int LA, int LB, bool INV, int OUTT, int NR_ = 2>
 struct TwoCfg {
@@ -352,6 +360,342 @@ k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, Two
       if (tid == 0) {
         signal_release(doneB + slot);
       }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K_TWO_TMA
+// Barrier-free two-level pass. Every item, A or B, is one 64 KB shared-memory
+// slot that arrives by TMA:
+//
+//   A item (g, n1): HBM tile [n2 < LA][16 combs] (4-D tensor map, 128-byte
+//                   swizzle) -> LA-point FFT of each comb by one half-warp
+//                   (radix 32 x 16, the exchange done in place in the slot
+//                   through an XOR-permuted row map, so only __syncwarp) ->
+//                   times W_L^{n1 k2} -> stored from registers to the group's
+//                   L2 scratch [n1][comb][k2] (16 lanes = one 128-byte line).
+//   B item (g, kb): scratch block [n1 < LB][16 combs][KB k2] (TMA from L2)
+//                   -> LB-point DFT over n1, optional W_M^{c k}, stored from
+//                   registers to HBM (lanes along the combs for natural
+//                   output, along k2 for the transposed one).
+//
+// Roles: warps 0..S-1 are loaders, loader s (lane 0) owning slot s: for the
+// CTA's items k = s, s + S, ... (global ids 2 blockIdx.x + (k & 1) +
+// 2 gridDim.x (k >> 1), a static deal with no counter) it waits for the item's dependencies,
+// then for the slot to be free, then issues the TMA and publishes the id.
+// Warps S.. are the 8 compute warps; they take the CTA's items in order,
+// wait on the slot's `full` mbarrier and arrive on its `empty` mbarrier
+// (count 8) as soon as they are done with the slot. No CTA or named barrier
+// is crossed. Items are ordered as in K_TWO (A items D groups ahead of the B
+// items of a group; a scratch slot is rewritten only after its previous
+// generation's B items have loaded it): every dependency has a smaller id and
+// each CTA runs its ids in increasing order, so with every CTA resident the
+// smallest unfinished id can always progress (no deadlock).
+//
+// A results are published per warp with a release reduction. Its MEMBAR is
+// deferred to just before the warp's next global stores (by then the stores
+// it orders have drained), or earlier if the warp would otherwise block on a
+// slot -- so a warp never waits on a release another CTA may need.
+template <int LA, int LB>
+struct TwoTmaCfg {
+  static constexpr int F = 16;
+  static constexpr int L = LA * LB;
+  static constexpr int KB = LA / LB;              // k2 values per B item
+  static constexpr int SLOT = LA * F;             // elements per item (A tile == B block)
+  static constexpr int SLOT_BYTES = SLOT * 8;     // 64 KB
+  static constexpr int S = 3;                     // slots
+  static constexpr int CW = 15;                   // compute warps (16 warps: 128 registers each)
+  static constexpr int THREADS = 32 * (1 + CW);
+  static constexpr int PAIRS = KB * F / 256;      // B (comb, k2) pairs per compute thread
+  static constexpr int SMEM = S * SLOT_BYTES + 2 * S * 8 + 1024;
+  static_assert(LA == 512, "A items are 512-point FFTs by half-warps (radix 32 x 16)");
+  static_assert(PAIRS * 256 == KB * F && KB % 16 == 0, "B item must tile 8 warps");
+};
+
+// 8-byte element (row, col) of a 128-byte-swizzled [rows][16] box
+__device__ __forceinline__ int sw128(int row, int col) {
+  return row * 16 + ((((col >> 1) ^ (row & 7)) << 1) | (col & 1));
+}
+
+__device__ __forceinline__ void tma_load_4d_hint(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                                 uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void signal_relaxed(unsigned* p) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// id -> (A or B, item index): DA A items, then A and B alternating, then the last B items
+__device__ __forceinline__ void two_decode(long long id, long long NA, long long DA, bool& isA, long long& idx) {
+  if (id < DA) {
+    isA = true;
+    idx = id;
+    return;
+  }
+  const long long r = id - DA, pairs = NA - DA;
+  if (r < 2 * pairs) {
+    isA = !(r & 1);
+    idx = isA ? DA + (r >> 1) : (r >> 1);
+  } else {
+    isA = false;
+    idx = pairs + (r - 2 * pairs);
+  }
+}
+
+template <int LA, int LB, bool INV, int OUTT, bool TWID>
+__global__ void __launch_bounds__(TwoTmaCfg<LA, LB>::THREADS, 1)
+k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tscr, float2* __restrict__ out,
+          TwoArgs a, const float2* __restrict__ tw, const float2* __restrict__ twl, const double2* __restrict__ wc,
+          const double2* __restrict__ wf, float scale) {
+  using Cfg = TwoTmaCfg<LA, LB>;
+  using V = float2;
+  constexpr int F = Cfg::F, S = Cfg::S, KB = Cfg::KB;
+  extern __shared__ unsigned char smem_raw[];
+  // 1024-byte alignment (128-byte swizzle atoms), by pointer arithmetic on the shared pointer
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  V* slots = reinterpret_cast<V*>(base);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + S * Cfg::SLOT_BYTES);
+  uint64_t* empty = full + S;
+  __shared__ long long s_id[S];
+  __shared__ unsigned s_unit, s_cnt[16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long NA = a.groups * LB, TOTAL = 2 * NA;
+  const long long DA = (long long)a.D * LB;  // A items handed out before the first B item
+  unsigned* workA = a.ctrl;
+  unsigned* doneA = a.ctrl + 1;
+  unsigned* doneB = a.ctrl + 1 + a.nslot;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    s_unit = 0;
+    for (int i = 0; i < 16; ++i) s_cnt[i] = 0;
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ============================================================ loader
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      // ids come from the global counter in order (each CTA runs its ids in increasing order);
+      // the next id is claimed one item ahead so the atomic's latency overlaps the current item.
+      // (Measured alternatives: claiming 4 ahead and issuing the oldest ready one -- 614 vs 530 us
+      // for 8192^2, claimed-but-unissued A items delay their group's B items; separate A and B
+      // streams -- no faster, and not deadlock-free in practice.)
+      long long nxt = (long long)atomicAdd(workA, 1u);
+      int k = 0;
+#pragma unroll 1
+      for (;; ++k) {
+        const int s = k % S;
+        const long long id = nxt;
+        if (id >= TOTAL) break;
+        nxt = (long long)atomicAdd(workA, 1u);
+        if (a.trace) { a.trace[id * 8 + 0] = gtimer(); a.trace[id * 8 + 6] = blockIdx.x; }
+        bool isA;
+        long long idx;
+        two_decode(id, NA, DA, isA, idx);
+        const long long g = idx / LB;
+        const int sub = (int)(idx % LB);
+        const int slot = (int)(g % a.nslot);
+        const unsigned gen = (unsigned)(g / a.nslot);
+        // dependency first (it does not need the slot), then the slot
+        if (isA) {
+          if (gen > 0) wait_geq(doneB + slot, gen * LB);
+        } else {
+          wait_geq(doneA + slot, (gen + 1) * LB);
+          fence_proxy_async_global();  // generic-proxy scratch stores -> our TMA reads
+        }
+        if (a.trace) a.trace[id * 8 + 1] = gtimer();
+        if (k >= S) mbar_wait(&empty[s], (uint32_t)(((k / S) - 1) & 1));
+        if (a.trace) { a.trace[id * 8 + 2] = gtimer(); a.trace[id * 8 + 7] = isA; }
+        s_id[s] = id * 2 + (isA ? 1 : 0);
+        V* dst = slots + s * Cfg::SLOT;
+        mbar_arrive_expect_tx(&full[s], Cfg::SLOT_BYTES);
+        if (isA) {
+          const long long b = g / a.chunks, ch = g % a.chunks;
+#pragma unroll 1
+          for (int r = 0; r < LA; r += 256)
+            tma_load_4d_hint(dst + r * F, &tin, (int)(ch * F), sub, r, (int)b, &full[s], pol);
+        } else {
+#pragma unroll 1
+          for (int h = 0; h < KB / 16; ++h)
+            tma_load_4d_l2(dst + h * LB * 16 * 16, &tscr, sub * KB + 16 * h, 0, 0, slot, &full[s]);
+        }
+      }
+      // end of work: terminal items k and k + 1 (the compute warps hold at most 15 units)
+#pragma unroll 1
+      for (int j = 0; j < 2; ++j, ++k) {
+        const int s = k % S;
+        if (k >= S) mbar_wait(&empty[s], (uint32_t)(((k / S) - 1) & 1));
+        s_id[s] = -1;
+        mbar_arrive(&full[s]);
+      }
+    }
+    return;
+  }
+
+  // ============================================================== compute
+  // Each item is 8 units (A: combs 2p, 2p+1; B: 1/8 of the pairs); compute warps take units in
+  // order from a shared counter, so any number of warps (up to 16) shares the items. At most 15
+  // units are outstanding, i.e. a warp is never two slot phases ahead of the loader.
+#pragma unroll 1
+  for (;;) {
+    unsigned u = 0;
+    if (lane == 0) u = atomicAdd(&s_unit, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    const int k = (int)(u >> 3), w = (int)(u & 7);
+    const int s = k % S;
+    mbar_wait(&full[s], (uint32_t)((k / S) & 1));
+    const long long code = s_id[s];  // id * 2 + isA, or -1 at the end
+    if (code < 0) break;
+    const long long id = code >> 1;
+    const bool isA = code & 1;
+    if (a.trace && w == 0 && lane == 0) a.trace[id * 8 + 3] = gtimer();
+    long long idx;
+    {
+      bool a_;
+      two_decode(id, NA, DA, a_, idx);
+    }
+    const long long g = idx / LB;
+    const int sub = (int)(idx % LB);
+    const int slot = (int)(g % a.nslot);
+    V* sl = slots + s * Cfg::SLOT;
+    if (isA) {
+      // ---- A: half-warp pairs (lanes 2t, 2t+1 = combs 2w, 2w+1 at the same t),
+      // so each half-warp's 64-bit accesses cover 8 distinct swizzle chunks
+      const int f = 2 * w + (lane & 1), t = lane >> 1;
+      V v[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) v[q] = sl[sw128(t + 16 * q, f)];
+      __syncwarp();
+      // element e = 32 a + c of the exchange lives in row 16 c + (a ^ (c & 7)):
+      // conflict-free for the writes (c fixed per register) and the reads (a fixed)
+      auto ex = [sl, f](int e) -> V& {
+        const int c = e & 31, a_ = e >> 5;
+        return sl[sw128(16 * c + (a_ ^ (c & 7)), f)];
+      };
+      auto release_slot = [&]() {
+        fence_proxy_async_smem();  // our generic writes before the next TMA write of the slot
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (a.trace && w == 0 && lane == 0) a.trace[id * 8 + 4] = gtimer();
+      };
+      SyncWarp sy;
+      if (a.diag == 1) release_slot();
+      else Stages<V, LA, 32, INV, 0>::run(v, t, ex, tw, sy, 0, release_slot);
+      // W_L^{n1 k2}, k2 = t + 16 i + 32 q (register 16 i + q) = W^{n1 (t + 16 i)} * W^{32 n1 q}
+      if (a.diag != 1 && sub > 0) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const V b0 = __ldg(twl + sub * (t + 16 * i));
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const V wq = q == 0 ? b0 : cmul(b0, __ldg(twl + 32 * sub * q));
+            v[16 * i + q] = ctw<INV>(v[16 * i + q], wq);
+          }
+        }
+      }
+      V* scr = a.scratch + (((size_t)slot * LB + sub) * F + f) * LA;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) __stcg(scr + out_index<LA, 32>(t, j), v[j]);
+      // the last of the item's 8 units publishes it (one release per A item)
+      __syncwarp();
+      if (lane == 0) {
+        unsigned old;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(old) : "r"(smem_u32(&s_cnt[k & 15])) : "memory");
+        if ((old & 7) == 7) {
+          if (a.diag == 3) signal_relaxed(doneA + slot);  // timing diagnostics only
+          else signal_release(doneA + slot);
+          if (a.trace) a.trace[id * 8 + 5] = gtimer();
+        }
+      }
+    } else {
+      // ---- B: LB-point DFTs over n1 for KB k2 values of 16 combs
+      if (w == 0 && lane == 0) signal_relaxed(doneB + slot);  // scratch block is in shared memory
+      const int kb = sub;
+      // pair p of this thread: OUTT=0 lanes = (8 combs x 2 k2) per half-warp; OUTT=1 lanes along k2
+      auto pair = [&](int m, int& f, int& k2l) {
+        if constexpr (OUTT == 0) {
+          const int hw = lane >> 4, l = lane & 15;
+          f = hw * 8 + (l >> 1);
+          k2l = (w + 8 * m) * 2 + (l & 1);
+        } else {
+          const int p = w * 32 + lane + 256 * m;
+          f = p / KB;
+          k2l = p % KB;
+        }
+      };
+      V v[Cfg::PAIRS][LB];
+#pragma unroll
+      for (int m = 0; m < Cfg::PAIRS; ++m) {
+        int f, k2l;
+        pair(m, f, k2l);
+#pragma unroll
+        for (int n1 = 0; n1 < LB; ++n1) v[m][n1] = sl[sw128(((k2l >> 4) * LB + n1) * 16 + f, k2l & 15)];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (a.trace && w == 0 && lane == 0) a.trace[id * 8 + 4] = gtimer();
+      const long long b = g / a.chunks, ch = g % a.chunks;
+#pragma unroll
+      for (int m = 0; m < Cfg::PAIRS; ++m) {
+        int f, k2l;
+        pair(m, f, k2l);
+        const int k2 = kb * KB + k2l;
+        V* u = v[m];
+        if (a.diag != 1) reg_dft<LB, INV>(u);
+        const long long c = ch * F + f;
+        if constexpr (TWID) {
+          constexpr int QA = LB / 4 > 0 ? LB / 4 : 1;
+          const double2 w0 = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)k2) & a.m_mask, a.fb);
+          const double2 s1 = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)LA) & a.m_mask, a.fb);
+          const double2 s2 = cmul(s1, s1), s4 = cmul(s2, s2);
+          const double2 w2 = cmul(w0, s2);
+          const V Bq[4] = {to_v(w0, (V*)nullptr), to_v(cmul(w0, s1), (V*)nullptr), to_v(w2, (V*)nullptr),
+                           to_v(cmul(w2, s1), (V*)nullptr)};
+          V Aq[QA];
+          {
+            double2 pw = make_double2(1.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < QA; ++q) {
+              Aq[q] = to_v(pw, (V*)nullptr);
+              if (q + 1 < QA) pw = cmul(pw, s4);
+            }
+          }
+#pragma unroll
+          for (int k1 = 0; k1 < LB; ++k1) u[k1] = ctw<INV>(u[k1], k1 < 4 ? Bq[k1 % 4] : cmul(Aq[k1 / 4], Bq[k1 % 4]));
+        }
+        if (scale != 1.0f) {
+#pragma unroll
+          for (int k1 = 0; k1 < LB; ++k1) u[k1] = mk(u[k1].x * scale, u[k1].y * scale);
+        }
+        if constexpr (OUTT == 0) {
+          V* o = out + b * a.bs_out + c;
+#pragma unroll
+          for (int k1 = 0; k1 < LB; ++k1) __stcs(o + (long long)(k2 + LA * k1) * a.es_out, u[k1]);
+        } else {
+          V* o = out + b * a.bs_out + c * a.es_out + k2;
+#pragma unroll
+          for (int k1 = 0; k1 < LB; ++k1) __stcs(o + LA * k1, u[k1]);
+        }
+      }
+      if (a.trace && w == 0 && lane == 0) a.trace[id * 8 + 5] = gtimer();
     }
   }
 }
