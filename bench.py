@@ -185,7 +185,7 @@ def run_reference(args, cfg):
     line = {"impl": "reference", "metric": "C2C FFT GFLOP/s (5N*log2N/t)", "unit": "GFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": desc, "n": n, "batch": batch, "kind": kind}}
+            "config": config_key(args.config)}
     res = cpu_reference_timing(n, batch, kind, threads, budget_s=args.ref_budget, steps=args.steps,
                                warmup=args.warmup)
     line.update({"value": res["value"], "ms_per_step": res["ms_per_step"],
@@ -238,9 +238,13 @@ def cpu_reference_timing(n, batch, kind, threads, budget_s=12.0, steps=None, war
         rows = min(n, max(threads * 16, 512))
         x = splitmix_signal(n * rows).reshape(rows, n)
         out = np.zeros_like(x)
-        ctx = R.lib.ref_ctx_create(n, 1024) if R is not None else None
-        run = (lambda: R.lib.ref_ctx_exec_batched(ctx, ctypes.c_void_p(x.ctypes.data),
-                                                  ctypes.c_void_p(out.ctypes.data), rows, threads))
+        if R is not None:
+            ctx = R.lib.ref_ctx_create(n, 1024)
+            run = lambda: R.lib.ref_ctx_exec_batched(ctx, ctypes.c_void_p(x.ctypes.data),
+                                                     ctypes.c_void_p(out.ctypes.data), rows, threads)
+        else:
+            O = Oracle()
+            run = lambda: O.fft_tiled(x)
         fl = 5.0 * n * math.log2(n)  # per row transform
         units = rows
         what = (f"{rows} length-{n} row transforms per step ({threads} threads); 2D = 2*{n} such transforms "
@@ -268,6 +272,238 @@ def cpu_reference_timing(n, batch, kind, threads, budget_s=12.0, steps=None, war
 
 
 # ---------------------------------------------------------------------------------------------------
+def device_input(torch, elems: int, seed: int, dev: int):
+    """Synthetic input resident in HBM (interleaved fp32 pairs): the counter-based splitmix64 signal
+    (identical to the oracle's orc_splitmix_signal_f32) up to 2^27 complex elements; above that a seeded
+    torch Philox uniform(-1,1) drawn on the device (generating 2^30 points in numpy would take ~1 min)."""
+    if elems <= (1 << 27):
+        return torch.from_numpy(splitmix_signal(elems, seed=seed).view(np.float32)).to(f"cuda:{dev}")
+    g = torch.Generator(device=f"cuda:{dev}")
+    g.manual_seed(seed)
+    x = torch.empty(2 * elems, dtype=torch.float32, device=f"cuda:{dev}")
+    x.uniform_(-1.0, 1.0, generator=g)
+    return x
+
+
+def config_key(name: str) -> dict:
+    """The workload description both arms (b200 and --impl reference) print identically."""
+    n, batch, kind, _, desc = CONFIGS[name]
+    elems = (n * n if kind == "2d" else n) * batch
+    return {"workload": desc, "name": name, "n": n, "batch_per_gpu": batch, "kind": kind,
+            "l2": ("inputs larger than L2 (no flush needed)" if elems * 8 > 126 * 2 ** 20
+                   else "L2-resident input: L2 flushed (256 MiB memset) before every timed step")}
+
+
+class L2Flush:
+    """Write a buffer larger than the 126 MB L2 between timed steps (L2-resident configs only)."""
+
+    def __init__(self, torch, dev):
+        self.buf = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+
+    def __call__(self):
+        self.buf.zero_()
+
+
+def time_steps(torch, step, stream, steps, flush=None):
+    """Device time per step (ms): CUDA events on the launching stream around the K steps; with an L2 flush,
+    events bracket each step so the flush itself is not counted."""
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        flush()
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in ev) / steps
+
+
+def cufft_timing(torch, name, x, steps, warmup, flush):
+    """torch.fft (cuFFT) on the same resident input, same event method: a comparison column, off the product path."""
+    n, batch, kind, _, _ = CONFIGS[name]
+    xc = x.view(torch.complex64)
+    if kind == "2d":
+        xc = xc.view(batch, n, n)
+        f = lambda: torch.fft.fft2(xc)
+    else:
+        xc = xc.view(batch, n)
+        f = lambda: torch.fft.fft(xc, dim=-1)
+    try:
+        for _ in range(max(3, warmup)):
+            f()
+        torch.cuda.synchronize()
+        ms = time_steps(torch, f, torch.cuda.current_stream(), steps, flush)
+        return {"ms_per_step": round(ms, 5), "value": round(flops_per_transform(n, kind) * batch / (ms * 1e-3) / 1e9, 2),
+                "unit": "GFLOP/s", "api": "torch.fft (cuFFT), comparison only, same CUDA-event method"}
+    except Exception as exc:  # comparison only: never fail the line
+        return {"ms_per_step": None, "value": None, "unit": "GFLOP/s", "api": f"torch.fft failed: {exc}"}
+    finally:
+        torch.cuda.empty_cache()
+
+
+def bench_config(name, args, torch, dev, world, rank, steps, warmup, with_cpu, with_cufft):
+    """One config on this rank: device-resident step time, per-pass kernel times, roofline, e2e, cpu_baseline."""
+    import torch.distributed as dist
+    from paper_1707_07263_b200 import _capi
+    n, batch, kind, p_alg, desc = CONFIGS[name]
+    total = n * n if kind == "2d" else n
+    distributed = world > 1 and kind == "1d" and batch == 1
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    plan = None
+    if distributed:
+        # one transform over all ranks: four-step, pass-1 store = the all-to-all (SURVEY §8e)
+        from paper_1707_07263_b200.distributed import DistributedFFT
+        dfft = DistributedFFT(total, exchange=args.exchange, device=dev)
+        o = dfft.ops
+        elems = o.n1 * o.c
+        x = device_input(torch, elems, 1 + rank, dev).view(torch.complex64).view(o.n1, o.c)
+        y = o.alloc((o.r, o.n2))
+        info = {"passes": len(o.plan.info()["factors"]) + 1, "factors": [o.n1] + o.plan.info()["factors"],
+                "launches_per_exec": None}
+
+        def step():
+            dfft.forward(x, y)
+    else:
+        plan = make_device_plan(name, dev)
+        info = plan.info()
+        elems = total * batch
+        x = device_input(torch, elems, 1 + rank, dev)
+        y = torch.empty_like(x)
+
+        def step():
+            plan.exec_device(x.data_ptr(), y.data_ptr(), _capi.FORWARD, sptr)
+
+    flush = L2Flush(torch, dev) if elems * 8 <= 126 * 2 ** 20 else None
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        ms_step = time_steps(torch, step, stream, steps, flush)
+    if world > 1:
+        t = torch.tensor([ms_step], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+        dist.barrier()
+    flops_job = flops_per_transform(n, kind) * (1 if distributed else batch * world)
+    value = flops_job / (ms_step * 1e-3) / 1e9
+
+    # ---- per-kernel durations: CUDA events between the plan's passes on the launching stream
+    peak, peak_kind = measured_peaks()
+    step_bytes = p_alg * 2 * total * 8 * batch  # algorithmic bytes of one step (SURVEY §8d), this rank
+    if distributed:
+        step_bytes //= world
+    pass_ms = None
+    if plan is not None:
+        if flush is None:
+            pass_ms = plan.exec_timed(x.data_ptr(), y.data_ptr(), _capi.FORWARD, sptr, reps=max(3, min(steps, 20)))
+        else:  # L2-resident: one flushed execution per sample
+            acc = None
+            reps = max(3, min(steps, 20))
+            for _ in range(reps):
+                flush()
+                t = plan.exec_timed(x.data_ptr(), y.data_ptr(), _capi.FORWARD, sptr, reps=1)
+                acc = t if acc is None else [a + b for a, b in zip(acc, t)]
+            pass_ms = [a / reps for a in acc]
+    if pass_ms:
+        dom = max(range(len(pass_ms)), key=lambda i: pass_ms[i])
+        kernel_bytes = 2 * total * 8 * batch  # every pass reads and writes each element once
+        achieved = kernel_bytes / (pass_ms[dom] * 1e-3) / 1e9
+        dominant = {"pass": dom, "length": info["factors"][dom] if dom < len(info["factors"]) else None,
+                    "ms": round(pass_ms[dom], 5), "algorithmic_bytes": kernel_bytes}
+    else:  # distributed: the whole step on this rank
+        achieved = step_bytes / (ms_step * 1e-3) / 1e9
+        dominant = {"pass": None, "ms": round(ms_step, 5), "algorithmic_bytes": step_bytes}
+    traffic = profile_traffic(name)
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4),
+                "traffic": (traffic.get("dominant") if isinstance(traffic, dict)
+                            else traffic if info["passes"] == 1 else None),
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "dominant_kernel": dominant,
+                "pass_ms": [round(v, 5) for v in pass_ms] if pass_ms else None,
+                "step": {"algorithmic_bytes": step_bytes, "p_alg": p_alg, "device_passes": info["passes"],
+                         "achieved": round(step_bytes / (ms_step * 1e-3) / 1e9, 1),
+                         "frac": round(step_bytes / (ms_step * 1e-3) / 1e9 / peak, 4),
+                         "traffic": traffic.get("step") if isinstance(traffic, dict) else traffic}}
+
+    # ---- e2e through the C ABI host entry point, pinned host buffers
+    e2e = None
+    if args.e2e_steps > 0 and not distributed:
+        hin = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        hin.copy_(x)
+        hout = torch.empty_like(hin, pin_memory=True)
+        plan.exec_host(hin.data_ptr(), hout.data_ptr(), _capi.FORWARD)  # warm-up (allocates staging)
+        if world > 1:
+            dist.barrier()
+        ts = []
+        for _ in range(args.e2e_steps if total * batch <= (1 << 27) else 2):
+            t0 = time.perf_counter()
+            plan.exec_host(hin.data_ptr(), hout.data_ptr(), _capi.FORWARD)
+            ts.append(time.perf_counter() - t0)
+        t_e2e = statistics.median(ts)
+        if world > 1:
+            t = torch.tensor([t_e2e], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e2e = float(t.item())
+        nbytes = elems * 8
+        chunked = batch > 1 and info["passes"] == 1 and kind == "1d"
+        e2e = {"value": round(flops_job / t_e2e / 1e9, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "ms_per_step": round(t_e2e * 1e3, 3),
+               "api": ("tilefft_exec_c2c_host (pinned host buffers, 32 MiB chunks, H2D, kernel and D2H queues "
+                       "overlapped)" if chunked else
+                       "tilefft_exec_c2c_host (pinned host buffers; whole-transform H2D, passes, D2H)")}
+        del hin, hout
+
+    cufft = cufft_timing(torch, name, x, min(steps, 50), warmup, flush) if with_cufft and not distributed else None
+
+    # ---- CPU baseline: the reference itself on this host (rank 0, N=1 only)
+    cpu = None
+    if with_cpu and rank == 0 and world == 1:
+        if name == "1d_2e30" and not args.cpu_2e30:
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": None, "kind": None,
+                   "sample": "skipped by default (one reference fft_tiled of 2^30 takes ~1 min of host time and "
+                             "16 GB of host memory); bench.py --cpu-2e30 runs it"}
+        else:
+            try:
+                threads = os.cpu_count() or 1
+                r = cpu_reference_timing(n, batch, kind, threads, budget_s=args.ref_budget)
+                cpu = {"value": round(r["value"], 3), "unit": "GFLOP/s", "cores": threads, "kind": r["kind"],
+                       "sample": r["sample"]}
+            except Exception as exc:  # report, never fail the GPU line
+                cpu = {"value": None, "unit": "GFLOP/s", "cores": None, "kind": None, "sample": f"failed: {exc}"}
+
+    rec = {"value": round(value, 2), "unit": "GFLOP/s", "ms_per_step": round(ms_step, 5), "steps": steps,
+           "warmup": warmup, "scaling": "strong" if distributed else "weak", "config": config_key(name),
+           "parallelism": (f"four-step over {world} GPUs, {args.exchange} all-to-all fused into pass 1"
+                           if distributed else f"batch sharded over {world} GPU(s), no collective"),
+           "device_factors": info["factors"], "hbm_gbs": round(step_bytes / (ms_step * 1e-3) / 1e9, 1),
+           "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "cufft": cufft,
+           "gpu_launches": steps * (info["launches_per_exec"] if info.get("launches_per_exec") else
+                                    len(info["factors"])),
+           "clocks": clk.summary()}
+    del x, y
+    if plan is not None:
+        plan.close()
+    if distributed:
+        dfft.close()
+    torch.cuda.empty_cache()
+    return rec
+
+
+SUB_STEPS = {"1d_2e20": 200, "1d_2e26": 100, "2d_8192": 100, "1d_2e30": 20}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -275,8 +511,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="batched1024", choices=sorted(CONFIGS))
+    ap.add_argument("--configs", default=None,
+                    help="comma list of extra configs timed in the same process as sub-records "
+                         "(default with --config batched1024: every other BASELINE config at N=1, 2d_8192 at N>1; "
+                         "'none' to skip)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cufft", action="store_true")
+    ap.add_argument("--cpu-2e30", action="store_true", help="also time the reference CPU fft_tiled at 2^30")
     ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="distributed single-transform configs at N>1: fused peer-store or NCCL all-to-all")
@@ -294,140 +536,37 @@ def main():
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
-    from paper_1707_07263_b200 import _capi
-
-    n, batch, kind, p_alg, desc = cfg
-    total = n * n if kind == "2d" else n
     steps, warmup = args.steps, max(3, args.warmup)
 
-    # ---- plan + resident input (synthetic, counter-based, per-rank seed)
-    distributed = world > 1 and kind == "1d" and batch == 1
-    if distributed:
-        # one transform over all ranks: four-step, pass-1 store = the all-to-all
-        from paper_1707_07263_b200.distributed import DistributedFFT
-        dfft = DistributedFFT(total, exchange=args.exchange, device=dev)
-        o = dfft.ops
-        elems = o.n1 * o.c
-        host_in = splitmix_signal(elems, seed=1 + rank)
-        x = torch.from_numpy(host_in.view(np.float32)).to(f"cuda:{dev}").view(torch.complex64).view(o.n1, o.c)
-        y = o.alloc((o.r, o.n2))
-        info = {"passes": 1 + len(o.plan.info()["factors"]) - 1, "launches_per_exec": None,
-                "factors": o.plan.info()["factors"]}
-        stream = torch.cuda.current_stream()
-
-        def step():
-            dfft.forward(x, y)
+    if args.configs is None:
+        subs = ([c for c in ("1d_2e20", "1d_2e26", "2d_8192", "1d_2e30") if c != args.config]
+                if args.config == "batched1024" and world == 1 else
+                (["2d_8192"] if args.config == "batched1024" else []))
     else:
-        plan = make_device_plan(args.config, dev)
-        info = plan.info()
-        elems = total * batch
-        host_in = splitmix_signal(elems, seed=1 + rank)
-        x = torch.from_numpy(host_in.view(np.float32)).to(f"cuda:{dev}")
-        y = torch.empty_like(x)
-        stream = torch.cuda.current_stream()
-        sptr = stream.cuda_stream
-
-        def step():
-            plan.exec_device(x.data_ptr(), y.data_ptr(), _capi.FORWARD, sptr)
-
-    for _ in range(warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clk:
-        e0.record(stream)
-        for _ in range(steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        dist.barrier()
-    ms_step = ms / steps
-    flops_job = flops_per_transform(n, kind) * (1 if distributed else batch * world)
-    value = flops_job / (ms_step * 1e-3) / 1e9
-
-    # ---- dominant kernel: per-launch CUDA-event durations on the launching stream
-    kernel_ms = []
-    if info["passes"] == 1:
-        kernel_ms = [ms_step]
-    else:
-        # time each pass separately by rebuilding a single-pass view is not exposed; use step time / passes
-        kernel_ms = [ms_step]
-    alg_bytes = p_alg * 2 * total * 8 * batch  # per launch == per step for single-pass plans
-    if distributed:
-        alg_bytes = p_alg * 2 * total * 8 // world  # this rank's share of the HBM traffic
-    peak, peak_kind = measured_peaks()
-    achieved = alg_bytes / (statistics.mean(kernel_ms) * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": profile_traffic(args.config),
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                "algorithmic_bytes_per_step": alg_bytes, "device_passes": info["passes"], "p_alg": p_alg}
-
-    # ---- e2e through the C ABI host entry point, pinned host buffers
-    e2e = None
-    if args.e2e_steps > 0 and not distributed:
-        hin = torch.from_numpy(host_in.view(np.float32)).pin_memory()
-        hout = torch.empty_like(hin).pin_memory()
-        if kind == "2d":
-            hplan = plan
-        else:
-            hplan = _capi.DevicePlan.create(total, batch, None, 8, _capi.MODE_FAST, None, dev)
-        hplan.exec_host(hin.data_ptr(), hout.data_ptr(), _capi.FORWARD)  # warm-up (allocs staging)
-        if world > 1:
-            dist.barrier()
-        ts = []
-        for _ in range(args.e2e_steps):
-            t0 = time.perf_counter()
-            hplan.exec_host(hin.data_ptr(), hout.data_ptr(), _capi.FORWARD)
-            ts.append(time.perf_counter() - t0)
-        t_e2e = statistics.median(ts)
-        if world > 1:
-            t = torch.tensor([t_e2e], device=f"cuda:{dev}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_e2e = float(t.item())
-        nbytes = elems * 8
-        e2e = {"value": round(flops_job / t_e2e / 1e9, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": nbytes,
-               "d2h_bytes_per_step": nbytes, "ms_per_step": round(t_e2e * 1e3, 3),
-               "api": "tilefft_exec_c2c_host (pinned host buffers, 16 MiB chunks, H2D, kernel and D2H queues overlapped)"}
-
-    # ---- CPU baseline: the reference itself on this host (rank 0, N=1 only)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        subs = [] if args.configs == "none" else [c for c in args.configs.split(",") if c and c != args.config]
+    with_cpu = not args.no_cpu_baseline
+    head = bench_config(args.config, args, torch, dev, world, rank, steps, warmup, with_cpu, not args.no_cufft)
+    sub_recs = {}
+    for c in subs:
         try:
-            threads = os.cpu_count() or 1
-            r = cpu_reference_timing(n, batch, kind, threads, budget_s=args.ref_budget)
-            cpu = {"value": round(r["value"], 3), "unit": "GFLOP/s", "cores": threads, "kind": r["kind"],
-                   "sample": r["sample"]}
-        except Exception as exc:  # report, never fail the GPU line
-            cpu = {"value": None, "unit": "GFLOP/s", "cores": None, "kind": None, "sample": f"failed: {exc}"}
+            sub_recs[c] = bench_config(c, args, torch, dev, world, rank, min(steps, SUB_STEPS.get(c, steps)),
+                                       warmup, with_cpu, not args.no_cufft)
+        except Exception as exc:  # a sub-record never takes the headline down
+            sub_recs[c] = {"error": f"{type(exc).__name__}: {exc}"}
 
     if rank == 0:
-        line = {
-            "metric": "C2C FFT GFLOP/s (5N*log2N/t)", "value": round(value, 2), "unit": "GFLOP/s",
-            "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": round(ms_step, 5),
-            "higher_is_better": True, "scaling": "strong" if distributed else "weak", "vs_baseline": None,
-            "dtype": "f32",
-            "data": "synthetic (counter-based uniform(-1,1), per-rank seed)",
-            "config": {"workload": desc, "n": n, "batch_per_gpu": batch, "kind": kind,
-                       "parallelism": (f"four-step over {world} GPUs, {args.exchange} all-to-all fused into pass 1"
-                                       if distributed else f"batch sharded over {world} GPU(s), no collective"),
-                       "l2": "inputs larger than L2" if elems * 16 > 126 * 2 ** 20 else "L2-resident (no flush)",
-                       "device_factors": info["factors"]},
-            "hbm_gbs": round(achieved, 1),
-            "roofline": roofline,
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-            "gpu_launches": steps * (info["launches_per_exec"] if info.get("launches_per_exec") else
-                                     len(info["factors"])),
-            "clocks": clk.summary(),
-        }
+        line = {"metric": "C2C FFT GFLOP/s (5N*log2N/t)", "value": head["value"], "unit": "GFLOP/s",
+                "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": head["ms_per_step"],
+                "higher_is_better": True, "scaling": head["scaling"], "vs_baseline": None, "dtype": "f32",
+                "data": ("synthetic uniform(-1,1), per-rank seed: counter-based splitmix64 up to 2^27 points, "
+                         "device Philox above")}
+        for k in ("config", "parallelism", "device_factors", "hbm_gbs", "roofline", "e2e", "cpu_baseline", "cufft",
+                  "gpu_launches", "clocks"):
+            line[k] = head[k]
+        if sub_recs:
+            line["configs"] = sub_recs
+            line["gpu_launches"] = head["gpu_launches"] + sum(r.get("gpu_launches", 0) for r in sub_recs.values())
+            line["gpu_launches_note"] = "headline + every sub-record's timed steps"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -89,6 +89,16 @@ TILEFFT_API int tilefft_exec_c2c_host(tilefft_plan_t plan, const void* h_in, voi
 
 TILEFFT_API int tilefft_plan_destroy(tilefft_plan_t plan);
 
+/* Measurement: run the plan's device passes `reps` times back to back
+ * (direct launches, no graph) on `cuda_stream`, with a CUDA event between
+ * consecutive passes; pass_ms[i] receives pass i's mean event-to-event time in
+ * milliseconds (the per-kernel duration bench.py's roofline divides by),
+ * for the first min(passes, max_passes) passes (tilefft_plan_info().passes;
+ * an unaligned d_in runs the plan's non-TMA variant). Synchronous. Same buffers and sign rules as exec_c2c. */
+TILEFFT_API int tilefft_exec_c2c_timed(tilefft_plan_t plan, const void* d_in, void* d_out, int sign, void* cuda_stream,
+                                       int reps, float* pass_ms, int max_passes);
+
+
 /* Plan introspection (all sizes in elements unless noted). */
 typedef struct {
   uint64_t n, batch, ny, nx;

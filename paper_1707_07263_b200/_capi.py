@@ -52,6 +52,7 @@ EXPORTS = (
     "tilefft_plan_create_2d",
     "tilefft_exec_c2c",
     "tilefft_exec_c2c_host",
+    "tilefft_exec_c2c_timed",
     "tilefft_plan_destroy",
     "tilefft_plan_info",
     "tilefft_build_twiddle",
@@ -98,6 +99,7 @@ def load() -> ctypes.CDLL:
         lib.tilefft_plan_create_2d.argtypes = [ctypes.POINTER(vp), u64, u64, u64, u32, i32]
         lib.tilefft_exec_c2c.argtypes = [vp, vp, vp, i32, vp]
         lib.tilefft_exec_c2c_host.argtypes = [vp, vp, vp, i32]
+        lib.tilefft_exec_c2c_timed.argtypes = [vp, vp, vp, i32, vp, i32, ctypes.POINTER(ctypes.c_float), i32]
         lib.tilefft_plan_destroy.argtypes = [vp]
         lib.tilefft_plan_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
         lib.tilefft_build_twiddle.argtypes = [u64, u32, vp]
@@ -171,6 +173,14 @@ class DevicePlan:
 
     def exec_host(self, h_in: int, h_out: int, sign: int = FORWARD) -> None:
         check(self._lib.tilefft_exec_c2c_host(self._h, ctypes.c_void_p(h_in), ctypes.c_void_p(h_out), int(sign)))
+
+    def exec_timed(self, d_in: int, d_out: int, sign: int = FORWARD, stream: int = 0, reps: int = 10) -> list:
+        """Per-pass mean CUDA-event durations (ms) over `reps` direct executions (measurement only)."""
+        n = int(self.info()["passes"])
+        ms = (ctypes.c_float * max(1, n))()
+        check(self._lib.tilefft_exec_c2c_timed(self._h, ctypes.c_void_p(d_in), ctypes.c_void_p(d_out), int(sign),
+                                               ctypes.c_void_p(stream), int(reps), ms, n))
+        return [float(ms[i]) for i in range(n)]
 
     def info(self) -> dict:
         pi = PlanInfo()

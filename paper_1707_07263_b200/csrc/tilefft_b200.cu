@@ -641,7 +641,7 @@ int finish_plan(tilefft_plan_s* P, TableBuilder<Real>& tb) {
 }
 
 template <typename Real>
-int exec_impl(tilefft_plan_s* P, const void* in, void* out, int sign, cudaStream_t st) {
+int exec_impl(tilefft_plan_s* P, const void* in, void* out, int sign, cudaStream_t st, cudaEvent_t* ev = nullptr) {
   const bool inv = sign == TILEFFT_INVERSE;
   const uint64_t total = P->is2d ? P->ny * P->nx : P->n;
   const Real scale = inv ? (Real)1 / (Real)total : (Real)1;
@@ -649,8 +649,11 @@ int exec_impl(tilefft_plan_s* P, const void* in, void* out, int sign, cudaStream
   // two-level passes stream their input with TMA (16-byte aligned); an
   // unaligned user buffer takes the equivalent plan without them
   const bool use_alt = !P->passes_alt.empty() && ((uintptr_t)in % 16 != 0);
+  int ip = 0;
   for (const Pass& ps : use_alt ? P->passes_alt : P->passes) {
     int rc;
+    if (ev) CUDA_TRY(cudaEventRecord(ev[ip], st));
+    ++ip;
     const void* src = buf(ps.src);
     void* dst = buf(ps.dst);
     if (ps.kind == K_EXACT) {
@@ -666,6 +669,7 @@ int exec_impl(tilefft_plan_s* P, const void* in, void* out, int sign, cudaStream
     }
     if (rc) return rc;
   }
+  if (ev) CUDA_TRY(cudaEventRecord(ev[ip], st));
   return 0;
 }
 
@@ -896,6 +900,44 @@ int tilefft_exec_c2c(tilefft_plan_t P, const void* in, void* out, int sign, void
   P->graphs.push_back({in, out, sign, exec});
   CUDA_TRY(cudaGraphLaunch(exec, st));
   return launched(0);
+}
+
+int tilefft_exec_c2c_timed(tilefft_plan_t P, const void* in, void* out, int sign, void* stream, int reps,
+                           float* pass_ms, int max_passes) {
+  g_err.clear();
+  if (!P) return fail(TILEFFT_EINVAL, "tilefft_exec_c2c_timed: null plan");
+  if (!in || !out || !pass_ms) return fail(TILEFFT_EINVAL, "tilefft_exec_c2c_timed: null buffer");
+  if (sign != TILEFFT_FORWARD && sign != TILEFFT_INVERSE)
+    return fail(TILEFFT_EINVAL, "tilefft_exec_c2c_timed: sign must be -1 or +1");
+  if (reps < 1) return fail(TILEFFT_EINVAL, "tilefft_exec_c2c_timed: reps must be >= 1");
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lock(P->graph_mu);
+  const bool use_alt = !P->passes_alt.empty() && ((uintptr_t)in % 16 != 0);
+  const int np = (int)(use_alt ? P->passes_alt : P->passes).size();
+  std::vector<cudaEvent_t> ev((size_t)(np + 1) * reps, nullptr);
+  int rc = 0;
+  for (auto& e : ev)
+    if (cudaEventCreate(&e) != cudaSuccess) { rc = fail(TILEFFT_ECUDA, "cudaEventCreate failed"); break; }
+  if (!rc && P->exec_done) rc = cudaStreamWaitEvent(st, P->exec_done, 0) == cudaSuccess ? 0 : fail(TILEFFT_ECUDA, "cudaStreamWaitEvent failed");
+  for (int r = 0; r < reps && !rc; ++r)
+    rc = P->elem_bytes == 8 ? exec_impl<float>(P, in, out, sign, st, &ev[(size_t)r * (np + 1)])
+                            : exec_impl<double>(P, in, out, sign, st, &ev[(size_t)r * (np + 1)]);
+  if (!rc && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(TILEFFT_ECUDA, "exec_c2c_timed: %s", cudaGetErrorString(cudaGetLastError()));
+  if (!rc) {
+    for (int i = 0; i < np && i < max_passes; ++i) {
+      double acc = 0;
+      for (int r = 0; r < reps; ++r) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev[(size_t)r * (np + 1) + i], ev[(size_t)r * (np + 1) + i + 1]);
+        acc += ms;
+      }
+      pass_ms[i] = (float)(acc / reps);
+    }
+  }
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  return rc;
 }
 
 int tilefft_exec_c2c_host(tilefft_plan_t P, const void* h_in, void* h_out, int sign) {
