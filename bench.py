@@ -366,8 +366,9 @@ def bench_config(name, args, torch, dev, world, rank, steps, warmup, with_cpu, w
         elems = o.n1 * o.c
         x = device_input(torch, elems, 1 + rank, dev).view(torch.complex64).view(o.n1, o.c)
         y = o.alloc((o.r, o.n2))
-        info = {"passes": len(o.plan.info()["factors"]) + 1, "factors": [o.n1] + o.plan.info()["factors"],
-                "launches_per_exec": None}
+        fac = o.plan.info()["factors"]  # [N1] + the local row plan's passes
+        info = {"passes": len(fac), "factors": fac,
+                "launches_per_exec": len(fac) + (1 if getattr(dfft, "device_barrier", False) else 0)}
 
         def step():
             dfft.forward(x, y)
@@ -424,6 +425,28 @@ def bench_config(name, args, torch, dev, world, rank, steps, warmup, with_cpu, w
     else:  # distributed: the whole step on this rank
         achieved = step_bytes / (ms_step * 1e-3) / 1e9
         dominant = {"pass": None, "ms": round(ms_step, 5), "algorithmic_bytes": step_bytes}
+    nvlink = None
+    if distributed:
+        # pass 1 alone (its epilogue IS the all-to-all): remote bytes / pass-1 time, max over ranks
+        reps = max(3, min(steps, 20))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(reps):
+            o.pass1(x, _capi.FORWARD)
+        b.record(stream)
+        torch.cuda.synchronize()
+        p1 = torch.tensor([a.elapsed_time(b) / reps], device=f"cuda:{dev}")
+        dist.all_reduce(p1, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        p1_ms = float(p1.item())
+        remote = (world - 1) * (o.n1 // world) * o.c * 8  # rows of this rank's pass-1 output owned by peers
+        nvlink = {"bytes_out_per_rank": remote, "pass1_ms": round(p1_ms, 5),
+                  "nvlink_gbs": round(remote / (p1_ms * 1e-3) / 1e9, 1),
+                  "peak_per_direction_gbs": 900.0, "exchange": args.exchange,
+                  "note": "pass-1 kernel time with the all-to-all fused into its stores (p2p), max over ranks"
+                          if args.exchange == "p2p" else "pass 1 + staging only; the NCCL all_to_all is separate"}
     traffic = profile_traffic(name)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4),
@@ -488,7 +511,7 @@ def bench_config(name, args, torch, dev, world, rank, steps, warmup, with_cpu, w
            "parallelism": (f"four-step over {world} GPUs, {args.exchange} all-to-all fused into pass 1"
                            if distributed else f"batch sharded over {world} GPU(s), no collective"),
            "device_factors": info["factors"], "hbm_gbs": round(step_bytes / (ms_step * 1e-3) / 1e9, 1),
-           "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "cufft": cufft,
+           "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "cufft": cufft, "nvlink": nvlink,
            "gpu_launches": steps * (info["launches_per_exec"] if info.get("launches_per_exec") else
                                     len(info["factors"])),
            "clocks": clk.summary()}
@@ -541,7 +564,7 @@ def main():
     if args.configs is None:
         subs = ([c for c in ("1d_2e20", "1d_2e26", "2d_8192", "1d_2e30") if c != args.config]
                 if args.config == "batched1024" and world == 1 else
-                (["2d_8192"] if args.config == "batched1024" else []))
+                (["2d_8192", "1d_2e30"] if args.config == "batched1024" else []))
     else:
         subs = [] if args.configs == "none" else [c for c in args.configs.split(",") if c and c != args.config]
     with_cpu = not args.no_cpu_baseline
@@ -561,7 +584,7 @@ def main():
                 "data": ("synthetic uniform(-1,1), per-rank seed: counter-based splitmix64 up to 2^27 points, "
                          "device Philox above")}
         for k in ("config", "parallelism", "device_factors", "hbm_gbs", "roofline", "e2e", "cpu_baseline", "cufft",
-                  "gpu_launches", "clocks"):
+                  "nvlink", "gpu_launches", "clocks"):
             line[k] = head[k]
         if sub_recs:
             line["configs"] = sub_recs

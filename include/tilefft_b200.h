@@ -145,10 +145,27 @@ TILEFFT_API int tilefft_dist_set_peers(tilefft_plan_t plan, void* const* dest, u
 TILEFFT_API int tilefft_dist_exec_pass1(tilefft_plan_t plan, const void* d_col_slab, int sign, void* cuda_stream);
 TILEFFT_API int tilefft_dist_exec_pass2(tilefft_plan_t plan, const void* d_row_slab, void* d_out, int sign,
                                         void* cuda_stream);
-/* CUDA IPC helpers for exchanging slab pointers between rank processes
- * (handle = 64 opaque bytes). */
-TILEFFT_API int tilefft_ipc_get_handle(const void* dptr, void* handle_out);
-TILEFFT_API int tilefft_ipc_open_handle(const void* handle, void** dptr);
+/* Device-side barrier for the distributed step. Each distributed plan owns a
+ * small device flag buffer; export it to the other ranks (tilefft_ipc_get_handle
+ * on the pointer tilefft_dist_flag_buffer returns), then give every plan all
+ * ranks' buffers in rank order, its own included. tilefft_dist_exec then runs
+ * pass 1 (peer stores) -> a one-thread barrier kernel (release-add on every
+ * rank's word, acquire-poll of its own) -> pass 2 on the row slab
+ * dest[rank] set by tilefft_dist_set_peers, all stream-ordered: no host
+ * synchronisation, capturable in a CUDA graph. Every rank must call it the
+ * same number of times; a rank that never arrives traps the waiting kernels
+ * after 60 s. */
+TILEFFT_API int tilefft_dist_flag_buffer(tilefft_plan_t plan, void** d_flags);
+TILEFFT_API int tilefft_dist_set_flags(tilefft_plan_t plan, void* const* d_flags, uint32_t nranks);
+TILEFFT_API int tilefft_dist_exec(tilefft_plan_t plan, const void* d_col_slab, void* d_out, int sign,
+                                  void* cuda_stream);
+
+/* CUDA IPC helpers for exchanging slab pointers between rank processes.
+ * A handle (64 opaque bytes) names the whole device allocation holding dptr;
+ * offset_out receives dptr's byte offset inside it (pointers from a caching
+ * allocator are sub-allocations), and open_handle returns base + offset. */
+TILEFFT_API int tilefft_ipc_get_handle(const void* dptr, void* handle_out, uint64_t* offset_out);
+TILEFFT_API int tilefft_ipc_open_handle(const void* handle, uint64_t offset, void** dptr);
 TILEFFT_API int tilefft_ipc_close_handle(void* dptr);
 
 /* Host-side root table with the reference's construction: entry j =

@@ -64,6 +64,9 @@ EXPORTS = (
     "tilefft_dist_set_peers",
     "tilefft_dist_exec_pass1",
     "tilefft_dist_exec_pass2",
+    "tilefft_dist_flag_buffer",
+    "tilefft_dist_set_flags",
+    "tilefft_dist_exec",
     "tilefft_ipc_get_handle",
     "tilefft_ipc_open_handle",
     "tilefft_ipc_close_handle",
@@ -111,8 +114,11 @@ def load() -> ctypes.CDLL:
         lib.tilefft_dist_set_peers.argtypes = [vp, ctypes.POINTER(vp), u32, u64, u64]
         lib.tilefft_dist_exec_pass1.argtypes = [vp, vp, i32, vp]
         lib.tilefft_dist_exec_pass2.argtypes = [vp, vp, vp, i32, vp]
-        lib.tilefft_ipc_get_handle.argtypes = [vp, vp]
-        lib.tilefft_ipc_open_handle.argtypes = [vp, ctypes.POINTER(vp)]
+        lib.tilefft_ipc_get_handle.argtypes = [vp, vp, ctypes.POINTER(u64)]
+        lib.tilefft_dist_flag_buffer.argtypes = [vp, ctypes.POINTER(vp)]
+        lib.tilefft_dist_set_flags.argtypes = [vp, ctypes.POINTER(vp), u32]
+        lib.tilefft_dist_exec.argtypes = [vp, vp, vp, i32, vp]
+        lib.tilefft_ipc_open_handle.argtypes = [vp, u64, ctypes.POINTER(vp)]
         lib.tilefft_ipc_close_handle.argtypes = [vp]
         lib.tilefft_last_error.restype = ctypes.c_char_p
         lib.tilefft_version.restype = ctypes.c_char_p
@@ -121,6 +127,7 @@ def load() -> ctypes.CDLL:
                      "tilefft_exchange",
                      "tilefft_interstage_scale", "tilefft_dist_plan_create", "tilefft_dist_layout",
                      "tilefft_dist_set_peers", "tilefft_dist_exec_pass1", "tilefft_dist_exec_pass2",
+                     "tilefft_dist_flag_buffer", "tilefft_dist_set_flags", "tilefft_dist_exec",
                      "tilefft_ipc_get_handle", "tilefft_ipc_open_handle", "tilefft_ipc_close_handle"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -258,17 +265,34 @@ class DistPlan(DevicePlan):
         check(self._lib.tilefft_dist_exec_pass2(self._h, ctypes.c_void_p(d_rows), ctypes.c_void_p(d_out), int(sign),
                                                 ctypes.c_void_p(stream)))
 
+    def flag_buffer(self) -> int:
+        p = ctypes.c_void_p()
+        check(self._lib.tilefft_dist_flag_buffer(self._h, ctypes.byref(p)))
+        return p.value
 
-def ipc_handle(dptr: int) -> bytes:
+    def set_flags(self, ptrs):
+        arr = (ctypes.c_void_p * len(ptrs))(*[int(p) for p in ptrs])
+        check(self._lib.tilefft_dist_set_flags(self._h, arr, len(ptrs)))
+
+    def exec_step(self, d_slab, d_out, sign=FORWARD, stream=0):
+        """pass 1 -> device barrier -> pass 2, stream-ordered (tilefft_dist_exec)."""
+        check(self._lib.tilefft_dist_exec(self._h, ctypes.c_void_p(d_slab), ctypes.c_void_p(d_out), int(sign),
+                                          ctypes.c_void_p(stream)))
+
+
+def ipc_handle(dptr: int):
+    """(64-byte CUDA IPC handle of the allocation holding dptr, byte offset of dptr inside it)."""
     buf = ctypes.create_string_buffer(64)
-    check(load().tilefft_ipc_get_handle(ctypes.c_void_p(dptr), buf))
-    return buf.raw
+    off = ctypes.c_uint64()
+    check(load().tilefft_ipc_get_handle(ctypes.c_void_p(dptr), buf, ctypes.byref(off)))
+    return buf.raw, off.value
 
 
-def ipc_open(handle: bytes) -> int:
+def ipc_open(handle) -> int:
+    raw, off = handle
     p = ctypes.c_void_p()
-    buf = ctypes.create_string_buffer(bytes(handle), 64)
-    check(load().tilefft_ipc_open_handle(buf, ctypes.byref(p)))
+    buf = ctypes.create_string_buffer(bytes(raw), 64)
+    check(load().tilefft_ipc_open_handle(buf, int(off), ctypes.byref(p)))
     return p.value
 
 

@@ -3,6 +3,7 @@
 // twiddle tables (the paper's precomputed "texture" roots),
 // the ping-pong workspace (tiled_fft.hpp:338-344) and the launch sequence of
 // one fft_tiled call (tiled_fft.hpp:346-405), one kernel per pass.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -166,6 +167,9 @@ struct tilefft_plan_s {
   uint64_t n1 = 0, n2 = 0;
   DistPass1 dist{};
   bool peers_set = false;
+  DevBuf flags;                   // [0] arrivals (written by every rank), [1] this rank's barrier epoch
+  unsigned* peer_flags[16] = {};  // every rank's arrival word (own included), set by tilefft_dist_set_flags
+  bool flags_set = false;
   tilefft_plan_s* inner = nullptr;  // row FFTs of length n2 over the rank's n1/nranks rows
   ~tilefft_plan_s() {
     if (inner) tilefft_plan_destroy(inner);
@@ -703,6 +707,42 @@ extern "C" TILEFFT_API long long tilefft_debug_two_trace(void* host, long long b
   return (long long)g_two_trace_bytes;
 }
 
+namespace {
+// Device-side barrier of the distributed step (replaces a host synchronize + a
+// process barrier between pass 1 and pass 2, so the step is stream-ordered and
+// graph-capturable). One thread: bump this rank's epoch, release-add 1 to every
+// rank's arrival word (the fence orders the preceding pass-1 peer stores, which
+// the kernel boundary already made happen-before this kernel), then acquire-poll
+// its own word until all ranks arrived for this epoch. The counters only grow,
+// so no reset is needed between calls; a peer that never arrives ends the wait
+// with a trap after 60 s instead of hanging the GPU.
+struct DistFlags {
+  unsigned* peer[16];
+  unsigned* mine;
+  unsigned* epoch;
+  int n;
+};
+__global__ void k_dist_barrier(DistFlags f) {
+  if (threadIdx.x != 0) return;
+  const unsigned e = *f.epoch + 1u;
+  *f.epoch = e;
+  __threadfence_system();
+  for (int d = 0; d < f.n; ++d) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(f.peer[d]) : "memory");
+  const unsigned target = e * (unsigned)f.n;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f.mine) : "memory");
+    if ((int)(v - target) >= 0) break;
+    __nanosleep(200);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 60ull * 1000000000ull) __trap();
+  }
+}
+}  // namespace
+
 extern "C" {
 
 const char* tilefft_last_error(void) { return g_err.c_str(); }
@@ -865,13 +905,19 @@ int tilefft_exec_c2c(tilefft_plan_t P, const void* in, void* out, int sign, void
   };
   std::lock_guard<std::mutex> lock(P->graph_mu);
   if (!P->exec_done) CUDA_TRY(cudaEventCreateWithFlags(&P->exec_done, cudaEventDisableTiming));
-  CUDA_TRY(cudaStreamWaitEvent(st, P->exec_done, 0));
+  // inside a caller's stream capture the graph's own edges order the execs (an
+  // event recorded outside the capture cannot be waited on from inside it)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(st, &cap));
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  if (!capturing) CUDA_TRY(cudaStreamWaitEvent(st, P->exec_done, 0));
   auto launched = [&](int rc) -> int {
     if (rc) return rc;
-    CUDA_TRY(cudaEventRecord(P->exec_done, st));
+    if (!capturing) CUDA_TRY(cudaEventRecord(P->exec_done, st));
     return 0;
   };
-  if (env_flag("TILEFFT_NO_GRAPH")) return launched(direct(st));
+  // a caller capturing its own graph gets the pass launches themselves captured
+  if (capturing || env_flag("TILEFFT_NO_GRAPH")) return launched(direct(st));
   for (auto& g : P->graphs)
     if (g.in == in && g.out == out && g.sign == sign) {
       CUDA_TRY(cudaGraphLaunch(g.exec, st));
@@ -1174,6 +1220,14 @@ int tilefft_dist_plan_create(tilefft_plan_t* out, uint64_t n, uint32_t nranks, u
     return rc;
   }
   for (uint64_t f : P->inner->dev_factors) P->dev_factors.push_back(f);
+  if (int frc = P->flags.alloc(256)) {
+    delete P;
+    return frc;
+  }
+  if (cudaMemset(P->flags.p, 0, 256) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+    delete P;
+    return fail(TILEFFT_ECUDA, "tilefft_dist_plan_create: clearing the barrier words failed");
+  }
   *out = P;
   return 0;
 }
@@ -1225,27 +1279,95 @@ int tilefft_dist_exec_pass2(tilefft_plan_t P, const void* d_rows, void* d_out, i
   return tilefft_exec_c2c(P->inner, d_rows, d_out, sign, stream);
 }
 
-int tilefft_ipc_get_handle(const void* dptr, void* handle_out) {
+int tilefft_dist_flag_buffer(tilefft_plan_t P, void** d_flags) {
   g_err.clear();
-  if (!dptr || !handle_out) return fail(TILEFFT_EINVAL, "tilefft_ipc_get_handle: null argument");
-  cudaIpcMemHandle_t h;
-  CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
-  std::memcpy(handle_out, &h, sizeof h);
+  if (!P || !P->is_dist) return fail(TILEFFT_EINVAL, "tilefft_dist_flag_buffer: not a distributed plan");
+  if (!d_flags) return fail(TILEFFT_EINVAL, "tilefft_dist_flag_buffer: null output");
+  *d_flags = P->flags.p;
   return 0;
 }
 
-int tilefft_ipc_open_handle(const void* handle, void** dptr) {
+int tilefft_dist_set_flags(tilefft_plan_t P, void* const* flags, uint32_t n) {
+  g_err.clear();
+  if (!P || !P->is_dist) return fail(TILEFFT_EINVAL, "tilefft_dist_set_flags: not a distributed plan");
+  if (!flags || n != P->nranks) return fail(TILEFFT_EINVAL, "tilefft_dist_set_flags: need one flag buffer per rank");
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!flags[i]) return fail(TILEFFT_EINVAL, "tilefft_dist_set_flags: null flag buffer");
+    P->peer_flags[i] = static_cast<unsigned*>(flags[i]);
+  }
+  if (flags[P->rank] != P->flags.p)
+    return fail(TILEFFT_EINVAL, "tilefft_dist_set_flags: entry %u must be this rank's own flag buffer", P->rank);
+  P->flags_set = true;
+  return 0;
+}
+
+int tilefft_dist_exec(tilefft_plan_t P, const void* d_slab, void* d_out, int sign, void* stream) {
+  g_err.clear();
+  if (!P || !P->is_dist) return fail(TILEFFT_EINVAL, "tilefft_dist_exec: not a distributed plan");
+  if (!P->flags_set) return fail(TILEFFT_EINVAL, "tilefft_dist_exec: barrier flags not set");
+  if (!d_out) return fail(TILEFFT_EINVAL, "tilefft_dist_exec: null output");
+  if (int rc = tilefft_dist_exec_pass1(P, d_slab, sign, stream)) return rc;
+  DistFlags f{};
+  for (uint32_t i = 0; i < P->nranks; ++i) f.peer[i] = P->peer_flags[i];
+  f.mine = static_cast<unsigned*>(P->flags.p);
+  f.epoch = f.mine + 1;
+  f.n = (int)P->nranks;
+  k_dist_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(f);
+  CUDA_TRY(cudaGetLastError());
+  return tilefft_exec_c2c(P->inner, P->dist.a.peers[P->rank], d_out, sign, stream);
+}
+
+namespace {
+// base of the device allocation holding p (CUDA IPC handles name whole
+// allocations; a caching allocator hands out pointers inside them)
+int alloc_base(const void* p, char** base) {
+  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<Fn>(f);
+  }();
+  if (!fn) return fail(TILEFFT_ECUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (CUdeviceptr)(uintptr_t)p) != CUDA_SUCCESS)
+    return fail(TILEFFT_EINVAL, "not a device allocation: %p", p);
+  *base = reinterpret_cast<char*>((uintptr_t)b);
+  return 0;
+}
+}  // namespace
+
+int tilefft_ipc_get_handle(const void* dptr, void* handle_out, uint64_t* offset_out) {
+  g_err.clear();
+  if (!dptr || !handle_out) return fail(TILEFFT_EINVAL, "tilefft_ipc_get_handle: null argument");
+  char* base = nullptr;
+  if (int rc = alloc_base(dptr, &base)) return rc;
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, base));
+  std::memcpy(handle_out, &h, sizeof h);
+  if (offset_out) *offset_out = (uint64_t)(static_cast<const char*>(dptr) - base);
+  return 0;
+}
+
+int tilefft_ipc_open_handle(const void* handle, uint64_t offset, void** dptr) {
   g_err.clear();
   if (!handle || !dptr) return fail(TILEFFT_EINVAL, "tilefft_ipc_open_handle: null argument");
   cudaIpcMemHandle_t h;
   std::memcpy(&h, handle, sizeof h);
-  CUDA_TRY(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  void* base = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *dptr = static_cast<char*>(base) + offset;
   return 0;
 }
 
 int tilefft_ipc_close_handle(void* dptr) {
   g_err.clear();
-  CUDA_TRY(cudaIpcCloseMemHandle(dptr));
+  char* base = nullptr;
+  if (int rc = alloc_base(dptr, &base)) return rc;
+  CUDA_TRY(cudaIpcCloseMemHandle(base));
   return 0;
 }
 

@@ -17,7 +17,11 @@
       transpose rides NVLink inside the kernel, overlapped tile by tile with the
       butterflies (the fused compute + all-to-all);
     - ``"nccl"``: pass 1 writes per-destination staging blocks, then one
-      ``all_to_all_single`` (NCCL grouped send/recv) and a local re-assembly.
+      ``all_to_all_single`` (NCCL grouped send/recv) and a local re-assembly
+      (one strided copy; the comparison path, not the product).
+  With GPU ops the p2p step is ``tilefft_dist_exec``: pass 1, a one-thread
+  peer-flag barrier kernel and pass 2 queued on one stream (no host
+  synchronisation, CUDA-graph capturable).
   Pass 2 is the row FFT of length N2 on the rank's row slab (local multi-pass).
 
 Layouts (rank g, C = N2/G, R = N1/G):
@@ -94,7 +98,17 @@ class GpuOps:
         self.torch.cuda.synchronize(self.device)
 
     def ipc_handle(self, t):
-        return _capi.ipc_handle(t.data_ptr())
+        return _capi.ipc_handle(t if isinstance(t, int) else t.data_ptr())
+
+    def flag_buffer(self):
+        return self.plan.flag_buffer()
+
+    def set_flags(self, ptrs):
+        self.plan.set_flags(ptrs)
+
+    def step(self, slab, out, sign):
+        """pass 1 (peer stores) -> device peer-flag barrier -> pass 2, no host synchronisation."""
+        self.plan.exec_step(slab.data_ptr(), out.data_ptr(), sign, self.stream())
 
     def ipc_open(self, h):
         return _capi.ipc_open(h)
@@ -138,6 +152,21 @@ class DistributedFFT:
                         ptrs.append(p)
                 self._dests.append(ptrs)
             o.set_dests(self._dests[0], o.n2, self.rank * o.c)
+            # device-side barrier words (GPU ops): every rank's flag buffer, own included
+            self.device_barrier = hasattr(o, "flag_buffer")
+            if self.device_barrier:
+                mine = o.flag_buffer()
+                handles = [None] * self.world
+                self.dist.all_gather_object(handles, o.ipc_handle(mine))
+                flags = []
+                for g, h in enumerate(handles):
+                    if g == self.rank:
+                        flags.append(mine)
+                    else:
+                        p = o.ipc_open(h)
+                        self._opened.append(p)
+                        flags.append(p)
+                o.set_flags(flags)
         elif self.exchange == "nccl":
             self.stage = o.alloc((self.world, o.r, o.c))
             self.recv = o.alloc((self.world, o.r, o.c))
@@ -156,14 +185,17 @@ class DistributedFFT:
             self._it += 1
             self.rows = self._slabs[b]
             o.set_dests(self._dests[b], o.n2, self.rank * o.c)
+            if self.device_barrier:
+                o.step(col_slab, out, sign)  # stream-ordered: no host sync, graph-capturable per slab parity
+                return out
         o.pass1(col_slab, sign)
         if self.exchange == "p2p":
             o.sync()              # this rank's peer stores are complete ...
             self.dist.barrier()   # ... and so are everyone else's into our slab
         elif self.exchange == "nccl":
             self.dist.all_to_all_single(self.recv, self.stage)
-            for s in range(self.world):  # [src][k1][c] -> [k1][src*C + c]
-                self.rows[:, s * o.c:(s + 1) * o.c] = self.recv[s]
+            # [src][k1][c] -> [k1][src*C + c]: one strided copy
+            self.rows.view(o.r, self.world, o.c).copy_(self.recv.permute(1, 0, 2))
         o.pass2(self.rows, out, sign)
         return out
 

@@ -282,3 +282,135 @@ def test_distributed_inverse_roundtrip_virtual_ranks(oracle):
     got_inv = run(X.astype(np.complex64), _capi.INVERSE)
     assert rel_l2(got_inv, want_inv) <= 1e-5 * 20
     assert rel_l2(got_inv, x) <= 1e-5 * 20
+
+
+def _virtual_step_setup(n, world):
+    """G virtual ranks on one B200 with two row slabs each and the device-barrier flags wired up."""
+    import torch
+    from paper_1707_07263_b200 import _capi
+    plans = [_capi.DistPlan.create_dist(n, world, g, 8, 0) for g in range(world)]
+    lay = plans[0].layout()
+    n2, c, r = lay["n2"], lay["cols_per_rank"], lay["rows_per_rank"]
+    slabs = [[torch.zeros((r, n2), dtype=torch.complex64, device="cuda") for _ in range(world)] for _ in range(2)]
+    flags = [p.flag_buffer() for p in plans]
+    for p in plans:
+        p.set_flags(flags)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    return plans, slabs, streams, n2, c, r
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,world", [(1 << 20, 2), (1 << 22, 4)])
+def test_distributed_device_barrier_virtual_ranks(oracle, n, world):
+    """tilefft_dist_exec (pass 1 -> peer-flag barrier kernel -> pass 2, no host sync) with every virtual rank on
+    its own stream, three back-to-back calls alternating the two row slabs, each vs the oracle."""
+    import torch
+    from paper_1707_07263_b200.distributed import assemble_output, column_slab
+    from oracle_lib import rel_l2
+    plans, slabs, streams, n2, c, r = _virtual_step_setup(n, world)
+    xs = [oracle.random_bench_signal(n, 20 + i).astype(np.complex64) for i in range(3)]
+    ins = [[torch.from_numpy(column_slab(x, world, g)).cuda() for g in range(world)] for x in xs]
+    outs = [[torch.empty((r, n2), dtype=torch.complex64, device="cuda") for _ in range(world)] for _ in xs]
+    torch.cuda.synchronize()
+    for i in range(3):
+        b = i & 1
+        for g, p in enumerate(plans):  # all calls queued without any host synchronisation
+            p.set_peers([t.data_ptr() for t in slabs[b]], n2, g * c)
+            p.exec_step(ins[i][g].data_ptr(), outs[i][g].data_ptr(), stream=streams[g].cuda_stream)
+    torch.cuda.synchronize()
+    for i, x in enumerate(xs):
+        got = assemble_output([o.cpu().numpy() for o in outs[i]], n)
+        err = rel_l2(got, oracle.fft_tiled(x))
+        assert err < 5e-7, (i, err)
+
+
+@pytest.mark.gpu
+def test_distributed_step_graph_capture_virtual_ranks(oracle):
+    """The distributed step is graph-capturable: each virtual rank's tilefft_dist_exec captured into a CUDA graph
+    (one per slab parity) and replayed gives the directly executed result bit for bit."""
+    import torch
+    from paper_1707_07263_b200.distributed import assemble_output, column_slab
+    from oracle_lib import rel_l2
+    n, world = 1 << 20, 2
+    plans, slabs, streams, n2, c, r = _virtual_step_setup(n, world)
+    x = oracle.random_bench_signal(n, 31).astype(np.complex64)
+    ins = [torch.from_numpy(column_slab(x, world, g)).cuda() for g in range(world)]
+    direct = [torch.empty((r, n2), dtype=torch.complex64, device="cuda") for _ in range(world)]
+    outs = [torch.empty((r, n2), dtype=torch.complex64, device="cuda") for _ in range(world)]
+    for g, p in enumerate(plans):  # direct run (also creates the inner plans' graphs)
+        p.set_peers([t.data_ptr() for t in slabs[0]], n2, g * c)
+        p.exec_step(ins[g].data_ptr(), direct[g].data_ptr(), stream=streams[g].cuda_stream)
+    for g, p in enumerate(plans):  # warm the (slab, out) pair the graphs will use
+        p.set_peers([t.data_ptr() for t in slabs[1]], n2, g * c)
+        p.exec_step(ins[g].data_ptr(), outs[g].data_ptr(), stream=streams[g].cuda_stream)
+    torch.cuda.synchronize()
+    graphs = []
+    for g, p in enumerate(plans):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=streams[g]):
+            p.set_peers([t.data_ptr() for t in slabs[1]], n2, g * c)
+            p.exec_step(ins[g].data_ptr(), outs[g].data_ptr(), stream=streams[g].cuda_stream)
+        graphs.append(gr)
+    torch.cuda.synchronize()
+    for rep in range(2):
+        for g in range(world):
+            with torch.cuda.stream(streams[g]):
+                graphs[g].replay()
+        torch.cuda.synchronize()
+        for g in range(world):
+            assert torch.equal(outs[g], direct[g]), (rep, g)
+    got = assemble_output([o.cpu().numpy() for o in outs], n)
+    assert rel_l2(got, oracle.fft_tiled(x)) < 5e-7
+
+
+def _ipc_worker(rank, world, port, n, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, os.path.dirname(HERE))
+    from paper_1707_07263_b200.distributed import DistributedFFT, column_slab
+    sys.path.insert(0, HERE)
+    from oracle_lib import Oracle
+    O = Oracle()
+    d = DistributedFFT(n, exchange="p2p", device=0)
+    assert d.device_barrier
+    outs = []
+    for seed in (41, 42, 43):  # both slabs of the double buffer, then the first again
+        x = O.random_bench_signal(n, seed).astype(np.complex64)
+        y = d.forward(torch.from_numpy(column_slab(x, world, rank)).cuda())
+        torch.cuda.synchronize()
+        outs.append(y.cpu().numpy())
+    gathered = [None] * world
+    dist.all_gather_object(gathered, outs)
+    if rank == 0:
+        q.put(gathered)
+    dist.barrier()
+    d.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_distributed_two_processes_cuda_ipc(oracle):
+    """Two real processes (gloo for the handle exchange, both on cuda:0): pass-1 stores land in the other process's
+    row slab through CUDA IPC and the device flag barrier orders them — the cross-process path of the p2p exchange
+    (on an 8-GPU box the same code maps peer GPUs' memory over NVLink)."""
+    import multiprocessing as mp
+    from paper_1707_07263_b200.distributed import assemble_output
+    from oracle_lib import rel_l2
+    n, world = 1 << 20, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    gathered = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for call, seed in enumerate((41, 42, 43)):
+        got = assemble_output([gathered[r][call] for r in range(world)], n)
+        want = oracle.fft_tiled(oracle.random_bench_signal(n, seed).astype(np.complex64))
+        assert rel_l2(got, want) < 5e-7, call
