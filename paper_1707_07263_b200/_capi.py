@@ -121,6 +121,7 @@ def load() -> ctypes.CDLL:
         lib.tilefft_ipc_open_handle.argtypes = [vp, u64, ctypes.POINTER(vp)]
         lib.tilefft_ipc_close_handle.argtypes = [vp]
         lib.tilefft_last_error.restype = ctypes.c_char_p
+        lib.tilefft_debug_two_watchdog.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), i32]  # diagnostics only
         lib.tilefft_version.restype = ctypes.c_char_p
         for name in ("tilefft_plan_create", "tilefft_plan_create_2d", "tilefft_exec_c2c", "tilefft_exec_c2c_host",
                      "tilefft_plan_destroy", "tilefft_plan_info", "tilefft_build_twiddle", "tilefft_account",

@@ -272,6 +272,30 @@ std::vector<uint64_t> balanced_factors(uint64_t n, uint64_t cap) {
 // ---------------------------------------------------------------- two-level passes
 // diagnostics: the last two-level pass created with TILEFFT_TWO_TRACE set
 unsigned long long* g_two_trace = nullptr;
+// host-mapped watchdog record shared by every two-level launch of the process
+// (written by the device only when a dependency wait times out, then it traps)
+unsigned long long* g_two_wd_host = nullptr;
+unsigned long long* g_two_wd_dev = nullptr;
+std::once_flag g_two_wd_once;
+unsigned long long* two_watchdog() {
+  std::call_once(g_two_wd_once, [] {
+    void* h = nullptr;
+    const size_t bytes = tfb::kWdWords * sizeof(unsigned long long);
+    if (cudaHostAlloc(&h, bytes, cudaHostAllocMapped) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    std::memset(h, 0, bytes);
+    void* d = nullptr;
+    if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    g_two_wd_host = static_cast<unsigned long long*>(h);
+    g_two_wd_dev = static_cast<unsigned long long*>(d);
+  });
+  return g_two_wd_dev;
+}
 size_t g_two_trace_bytes = 0;
 bool env_flag(const char* name) {
   const char* e = std::getenv(name);
@@ -317,13 +341,15 @@ Pass make_two_pass(tilefft_plan_s* P, TableBuilder<Real>& tb, uint64_t L, long l
   a.bs_in = bs_in;
   a.bs_out = bs_out;
   a.es_out = es_out;
-  a.D = std::max(1, env_int("TILEFFT_TWO_D", 24));
+  // lag / ring defaults from the sweep in DESIGN.md §8 (8192^2 columns: D 40, 56 slots best)
+  a.D = std::max(1, env_int("TILEFFT_TWO_D", 40));
   if (a.D > a.groups) a.D = (int)a.groups;
-  a.nslot = std::max(a.D + 1, env_int("TILEFFT_TWO_NSLOT", 2 * a.D));
+  a.nslot = std::max(a.D + 1, env_int("TILEFFT_TWO_NSLOT", a.D + 16));
   a.discard = env_int("TILEFFT_TWO_DISCARD", 1);
   ps.two_kernel = env_int("TILEFFT_TWO_KERNEL", 1);
   a.diag = env_int("TILEFFT_TWO_DIAG", 0);
   a.trace = nullptr;
+  a.watchdog = two_watchdog();
   if (env_flag("TILEFFT_TWO_TRACE")) {  // diagnostics: per-item timestamps, read by tilefft_debug_two_trace
     const size_t bytes = (size_t)a.groups * ps.lb * 2 * 8 * sizeof(unsigned long long);
     if (cudaMalloc(&a.trace, bytes) == cudaSuccess) {
@@ -697,6 +723,16 @@ int with_device_buffers(int device, const void* h_in, void* h_out, size_t in_byt
 // ================================================================ C ABI
 // Diagnostics only (not part of include/tilefft_b200.h): copy the per-item timestamps of the
 // last traced two-level pass (TILEFFT_TWO_TRACE=1) to host memory; returns the bytes available.
+// Diagnostics only: the watchdog record of the last two-level dependency wait that timed
+// out (tfb::kWdWords words, layout in twolevel.cuh); returns 0 if none fired.
+extern "C" TILEFFT_API int tilefft_debug_two_watchdog(unsigned long long* out, int words) {
+  if (!g_two_wd_host) return 0;
+  volatile unsigned long long* w = g_two_wd_host;
+  if (out)
+    for (int i = 0; i < words && i < tfb::kWdWords; ++i) out[i] = w[i];
+  return w[0] ? 1 : 0;
+}
+
 extern "C" TILEFFT_API long long tilefft_debug_two_trace(void* host, long long bytes) {
   if (!g_two_trace) return 0;
   if (host && bytes > 0) {

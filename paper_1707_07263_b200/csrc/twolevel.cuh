@@ -43,6 +43,7 @@ struct TwoArgs {
   float2* scratch;           // nslot * L * 16 elements
   unsigned* ctrl;            // [0] work counter, [1..nslot] A done, [nslot+1..2 nslot] B done
   unsigned long long* trace; // diagnostics (TILEFFT_TWO_TRACE): 8 timestamps per item id, else null
+  unsigned long long* watchdog;  // host-mapped record of a dependency wait that timed out (see wait_geq_wd)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -98,6 +99,66 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
 }
 __device__ __forceinline__ void wait_geq(const unsigned* p, unsigned v) {
   while (ld_relaxed_u32(p) < v) __nanosleep(40);
+}
+// Watchdog for the persistent two-level kernels: a dependency that is not met
+// within 10 s is a protocol failure, not a slow peer (the kernel runs for
+// < 1 ms per GB). The waiter that times out records what it awaited into
+// host-mapped memory (it survives the context), asks every other waiting
+// thread to record its own state (`dump`), then traps -- so a bug surfaces
+// as a launch error with a per-CTA snapshot instead of a hung GPU.
+// wd: [0] fired, [1] block, [2] item id, [3] awaited, [4] seen, [5] what
+// (1 = A slot reuse, 2 = B inputs), [7] dump request; per CTA b at
+// [8 + 4b]: the id a waiting loader holds, what it waits for (1/2), awaited<<32|seen.
+constexpr int kWdWords = 8 + 4 * 256;
+__device__ __forceinline__ unsigned long long wd_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void wd_record(unsigned long long* wd, int slot_word, unsigned long long v) {
+  if (wd && blockIdx.x < 256) reinterpret_cast<volatile unsigned long long*>(wd)[8 + 4 * blockIdx.x + slot_word] = v;
+}
+__device__ __forceinline__ bool wd_dump_requested(unsigned long long* wd) {
+  return wd && reinterpret_cast<volatile unsigned long long*>(wd)[7] != 0;
+}
+static __device__ __noinline__ void wd_fire(unsigned long long* wd, long long id, unsigned v, unsigned seen, int what) {
+  if (wd) {
+    volatile unsigned long long* w = wd;
+    w[1] = blockIdx.x;
+    w[2] = (unsigned long long)id;
+    w[3] = v;
+    w[4] = seen;
+    w[5] = (unsigned long long)what;
+    __threadfence_system();
+    w[7] = 1;  // everyone else: record your state
+    __threadfence_system();
+    const unsigned long long t0 = wd_now();
+    while (wd_now() - t0 < 300ull * 1000000ull) __nanosleep(1000);
+    w[0] = 1;
+    __threadfence_system();
+  }
+  __trap();
+}
+__device__ __forceinline__ void wait_geq_wd(const unsigned* p, unsigned v, unsigned long long* wd, long long id,
+                                            int what) {
+  unsigned long long t0 = 0;  // the timer is read only once a wait has lasted ~1024 polls
+  bool dumped = false;
+  for (unsigned it = 1;; ++it) {
+    const unsigned seen = ld_relaxed_u32(p);
+    if (seen >= v) return;
+    __nanosleep(40);
+    if ((it & 1023u) == 0) {
+      if (!dumped && wd_dump_requested(wd)) {
+        wd_record(wd, 0, (unsigned long long)id);
+        wd_record(wd, 1, (unsigned long long)what);
+        wd_record(wd, 2, ((unsigned long long)v << 32) | seen);
+        dumped = true;
+      }
+      const unsigned long long t = wd_now();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 10ull * 1000000000ull) wd_fire(wd, id, v, seen, what);
+    }
+  }
 }
 __device__ __forceinline__ void signal_release(unsigned* p) {
   asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
@@ -241,7 +302,7 @@ k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, Two
           v[j] = ctw<INV>(v[j], __ldg(twl + n1 * k2));
         }
       }
-      if (tid == 0 && gen > 0) wait_geq(doneB + slot, gen * LB);
+      if (tid == 0 && gen > 0) wait_geq_wd(doneB + slot, gen * LB, a.watchdog, -1, 1);
       sy();
       if constexpr (OUTT == 0) {
 #pragma unroll
@@ -264,7 +325,7 @@ k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, Two
         s_b_id = id;
         if (id < NA) {
           const long long g = id / LB;
-          wait_geq(doneA + (int)(g % a.nslot), (unsigned)(g / a.nslot + 1) * LB);
+          wait_geq_wd(doneA + (int)(g % a.nslot), (unsigned)(g / a.nslot + 1) * LB, a.watchdog, id, 2);
         }
       }
       sy();
@@ -470,7 +531,15 @@ k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUten
   uint64_t* full = reinterpret_cast<uint64_t*>(base + S * Cfg::SLOT_BYTES);
   uint64_t* empty = full + S;
   __shared__ long long s_id[S];
-  __shared__ unsigned s_unit, s_cnt[16];
+  // s_seq[s]: CTA-local index of the item the loader last put in slot s. TMA loads land out of order, so a
+  // compute warp can reach item k + S while item k (same slot) is still in flight; a parity wait for the
+  // later phase would then return at once (the barrier's phases alias mod 2). The warp therefore first sees
+  // its own item index in s_seq (written only after item k - S was released, i.e. its phase completed), then waits.
+  __shared__ int s_seq[S];
+  // s_cnt[k & 31]: finished units of A item k; its last unit resets the word, and the loader issues an A item
+  // only into a zero word, so a unit that lags far behind (it released its slot before its stores) can never
+  // count toward a later item that shares the word
+  __shared__ unsigned s_unit, s_cnt[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long NA = a.groups * LB, TOTAL = 2 * NA;
   const long long DA = (long long)a.D * LB;  // A items handed out before the first B item
@@ -483,7 +552,8 @@ k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUten
       mbar_init(&empty[s], 8);
     }
     s_unit = 0;
-    for (int i = 0; i < 16; ++i) s_cnt[i] = 0;
+    for (int i = 0; i < S; ++i) s_seq[i] = -1;
+    for (int i = 0; i < 32; ++i) s_cnt[i] = 0;
     mbar_fence_init();
   }
   __syncthreads();
@@ -515,15 +585,20 @@ k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUten
         const unsigned gen = (unsigned)(g / a.nslot);
         // dependency first (it does not need the slot), then the slot
         if (isA) {
-          if (gen > 0) wait_geq(doneB + slot, gen * LB);
+          if (gen > 0) wait_geq_wd(doneB + slot, gen * LB, a.watchdog, id, 1);
         } else {
-          wait_geq(doneA + slot, (gen + 1) * LB);
+          wait_geq_wd(doneA + slot, (gen + 1) * LB, a.watchdog, id, 2);
           fence_proxy_async_global();  // generic-proxy scratch stores -> our TMA reads
         }
         if (a.trace) a.trace[id * 8 + 1] = gtimer();
-        if (k >= S) mbar_wait(&empty[s], (uint32_t)(((k / S) - 1) & 1));
+        if (k >= S) {
+          mbar_wait(&empty[s], (uint32_t)(((k / S) - 1) & 1));
+        }
         if (a.trace) { a.trace[id * 8 + 2] = gtimer(); a.trace[id * 8 + 7] = isA; }
+        if (isA)
+          while (*reinterpret_cast<volatile unsigned*>(&s_cnt[k & 31]) != 0) __nanosleep(20);
         s_id[s] = id * 2 + (isA ? 1 : 0);
+        *reinterpret_cast<volatile int*>(&s_seq[s]) = k;
         V* dst = slots + s * Cfg::SLOT;
         mbar_arrive_expect_tx(&full[s], Cfg::SLOT_BYTES);
         if (isA) {
@@ -543,6 +618,7 @@ k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUten
         const int s = k % S;
         if (k >= S) mbar_wait(&empty[s], (uint32_t)(((k / S) - 1) & 1));
         s_id[s] = -1;
+        *reinterpret_cast<volatile int*>(&s_seq[s]) = k;
         mbar_arrive(&full[s]);
       }
     }
@@ -560,6 +636,7 @@ k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUten
     u = __shfl_sync(0xffffffffu, u, 0);
     const int k = (int)(u >> 3), w = (int)(u & 7);
     const int s = k % S;
+    while (*reinterpret_cast<volatile int*>(&s_seq[s]) != k) __nanosleep(32);
     mbar_wait(&full[s], (uint32_t)((k / S) & 1));
     const long long code = s_id[s];  // id * 2 + isA, or -1 at the end
     if (code < 0) break;
@@ -618,8 +695,9 @@ k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUten
       if (lane == 0) {
         unsigned old;
         asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
-                     : "=r"(old) : "r"(smem_u32(&s_cnt[k & 15])) : "memory");
-        if ((old & 7) == 7) {
+                     : "=r"(old) : "r"(smem_u32(&s_cnt[k & 31])) : "memory");
+        if (old == 7) {
+          asm volatile("st.relaxed.cta.shared::cta.u32 [%0], 0;" ::"r"(smem_u32(&s_cnt[k & 31])) : "memory");
           if (a.diag == 3) signal_relaxed(doneA + slot);  // timing diagnostics only
           else signal_release(doneA + slot);
           if (a.trace) a.trace[id * 8 + 5] = gtimer();
@@ -649,6 +727,7 @@ k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUten
 #pragma unroll
         for (int n1 = 0; n1 < LB; ++n1) v[m][n1] = sl[sw128(((k2l >> 4) * LB + n1) * 16 + f, k2l & 15)];
       }
+      fence_proxy_async_smem();  // our generic reads of the slot before the next TMA write of it
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (a.trace && w == 0 && lane == 0) a.trace[id * 8 + 4] = gtimer();

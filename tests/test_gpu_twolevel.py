@@ -169,3 +169,28 @@ def test_two_level_2d_8192_square_roundtrip(tf, oracle):
         wy = np.exp(-2j * np.pi * (ky * np.arange(ny) % ny) / ny)
         exact = wy @ (x64 @ wx)  # separable direct sum, fp64
         assert abs(spec[ky, kx] - exact) <= 1e-5 * math.log2(ny * nx) * np.sqrt(e_x), (ky, kx)
+
+
+def test_two_level_repeated_runs_stress(tf, oracle, monkeypatch):
+    """Many back-to-back two-level passes under the lag/slot settings that once exposed a slot-phase race
+    (a compute warp could wait on the next phase of a slot whose TMA had not landed yet; s_seq now orders it):
+    every run bit-identical to the first; a protocol hang would surface as the watchdog's launch error."""
+    import torch
+    from paper_1707_07263_b200 import _capi
+    n = 8192
+    img = torch.from_numpy(oracle.random_bench_signal(n * n, 9).astype(np.complex64)).cuda()
+    out = torch.empty_like(img)
+    st = torch.cuda.current_stream().cuda_stream
+    for d, slots in [(40, 56), (80, 96), (24, 48)]:
+        monkeypatch.setenv("TILEFFT_TWO_D", str(d))
+        monkeypatch.setenv("TILEFFT_TWO_NSLOT", str(slots))
+        dp = _capi.DevicePlan.create_2d(n, n, 1, 8, 0)
+        dp.exec_device(img.data_ptr(), out.data_ptr(), _capi.FORWARD, st)
+        ref = out.clone()
+        for _ in range(60):
+            dp.exec_device(img.data_ptr(), out.data_ptr(), _capi.FORWARD, st)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref), (d, slots)
+        dp.close()
+    wd = (__import__("ctypes").c_ulonglong * 8)()
+    assert _capi.load().tilefft_debug_two_watchdog(wd, 8) == 0

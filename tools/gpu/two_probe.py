@@ -15,13 +15,37 @@ if len(sys.argv) > 2 and sys.argv[1] == "--child":
     x = torch.randn(n, dtype=torch.complex64, device="cuda"); y = torch.empty_like(x)
     st = torch.cuda.current_stream().cuda_stream
     f = lambda: dp.exec_device(x.data_ptr(), y.data_ptr(), _capi.FORWARD, st)
-    for _ in range(3): f()
-    torch.cuda.synchronize()
+    try:
+        for _ in range(3): f()
+        torch.cuda.synchronize()
+    except Exception as exc:
+        import ctypes
+        lib = _capi.load()
+        w = (ctypes.c_ulonglong * 1032)()
+        fired = lib.tilefft_debug_two_watchdog(w, 1032)
+        print(f"{case} ERROR {str(exc)[:80]} watchdog={fired} record={list(w[:8])}", flush=True)
+        for b in range(256):
+            r = list(w[8 + 4 * b: 12 + 4 * b])
+            if any(r):
+                print(f"  cta {b}: waiting id {r[0]} what {r[1]} need/seen {r[2] >> 32}/{r[2] & 0xffffffff}", flush=True)
+        sys.exit(1)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = int(os.environ.get("REPS", "20"))
     a.record()
-    for _ in range(reps): f()
-    b.record(); torch.cuda.synchronize()
+    try:
+        for _ in range(reps): f()
+        b.record(); torch.cuda.synchronize()
+    except Exception as exc:
+        import ctypes
+        lib = _capi.load()
+        w = (ctypes.c_ulonglong * 1032)()
+        fired = lib.tilefft_debug_two_watchdog(w, 1032)
+        print(f"{case} ERROR {str(exc)[:80]} watchdog={fired} record={list(w[:8])}", flush=True)
+        for b in range(256):
+            r = list(w[8 + 4 * b: 12 + 4 * b])
+            if any(r):
+                print(f"  cta {b}: waiting id {r[0]} what {r[1]} need/seen {r[2] >> 32}/{r[2] & 0xffffffff}", flush=True)
+        sys.exit(1)
     print(f"{case} factors {dp.info()['factors']}: {a.elapsed_time(b) / reps * 1e3:.1f} us", flush=True)
     sys.exit(0)
 cases = json.loads(sys.argv[1])
@@ -33,7 +57,8 @@ for v in variants:
         try:
             r = subprocess.run([sys.executable, __file__, "--child", json.dumps(c)], env=env, capture_output=True,
                                text=True, timeout=int(os.environ.get("CASE_TIMEOUT", "90")))
-            out = (r.stdout.strip().splitlines() or [r.stderr.strip()[-300:]])[-1]
+            lines = r.stdout.strip().splitlines() or [r.stderr.strip()[-300:]]
+            out = lines[-1] if "ERROR" not in r.stdout else "\n".join(lines)
         except subprocess.TimeoutExpired:
             out = f"{c}: TIMEOUT (hang)"
         print(v, out, flush=True)
