@@ -304,6 +304,14 @@ class L2Flush:
         self.buf.zero_()
 
 
+def max_over_ranks(torch, dist, v: float, dev: int) -> float:
+    """MAX of a per-rank scalar over the job (a CUDA tensor for NCCL, a host tensor for gloo)."""
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{dev}" if on_gpu else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def time_steps(torch, step, stream, steps, flush=None):
     """Device time per step (ms): CUDA events on the launching stream around the K steps; with an L2 flush,
     events bracket each step so the flush itself is not counted."""
@@ -392,9 +400,7 @@ def bench_config(name, args, torch, dev, world, rank, steps, warmup, with_cpu, w
     with ClockSampler(dev) as clk:
         ms_step = time_steps(torch, step, stream, steps, flush)
     if world > 1:
-        t = torch.tensor([ms_step], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
+        ms_step = max_over_ranks(torch, dist, ms_step, dev)
         dist.barrier()
     flops_job = flops_per_transform(n, kind) * (1 if distributed else batch * world)
     value = flops_job / (ms_step * 1e-3) / 1e9
@@ -437,10 +443,8 @@ def bench_config(name, args, torch, dev, world, rank, steps, warmup, with_cpu, w
             o.pass1(x, _capi.FORWARD)
         b.record(stream)
         torch.cuda.synchronize()
-        p1 = torch.tensor([a.elapsed_time(b) / reps], device=f"cuda:{dev}")
-        dist.all_reduce(p1, op=dist.ReduceOp.MAX)
+        p1_ms = max_over_ranks(torch, dist, a.elapsed_time(b) / reps, dev)
         dist.barrier()
-        p1_ms = float(p1.item())
         remote = (world - 1) * (o.n1 // world) * o.c * 8  # rows of this rank's pass-1 output owned by peers
         nvlink = {"bytes_out_per_rank": remote, "pass1_ms": round(p1_ms, 5),
                   "nvlink_gbs": round(remote / (p1_ms * 1e-3) / 1e9, 1),
@@ -450,7 +454,7 @@ def bench_config(name, args, torch, dev, world, rank, steps, warmup, with_cpu, w
     traffic = profile_traffic(name)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4),
-                "traffic": (traffic.get("dominant") if isinstance(traffic, dict)
+                "traffic": (None if distributed else traffic.get("dominant") if isinstance(traffic, dict)
                             else traffic if info["passes"] == 1 else None),
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                 "dominant_kernel": dominant,
@@ -458,7 +462,8 @@ def bench_config(name, args, torch, dev, world, rank, steps, warmup, with_cpu, w
                 "step": {"algorithmic_bytes": step_bytes, "p_alg": p_alg, "device_passes": info["passes"],
                          "achieved": round(step_bytes / (ms_step * 1e-3) / 1e9, 1),
                          "frac": round(step_bytes / (ms_step * 1e-3) / 1e9 / peak, 4),
-                         "traffic": traffic.get("step") if isinstance(traffic, dict) else traffic}}
+                         "traffic": (None if distributed else traffic.get("step") if isinstance(traffic, dict)
+                                     else traffic)}}
 
     # ---- e2e through the C ABI host entry point, pinned host buffers
     e2e = None
@@ -476,9 +481,7 @@ def bench_config(name, args, torch, dev, world, rank, steps, warmup, with_cpu, w
             ts.append(time.perf_counter() - t0)
         t_e2e = statistics.median(ts)
         if world > 1:
-            t = torch.tensor([t_e2e], device=f"cuda:{dev}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_e2e = float(t.item())
+            t_e2e = max_over_ranks(torch, dist, t_e2e, dev)
         nbytes = elems * 8
         chunked = batch > 1 and info["passes"] == 1 and kind == "1d"
         e2e = {"value": round(flops_job / t_e2e / 1e9, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": nbytes,
@@ -554,8 +557,15 @@ def main():
     import torch.distributed as dist
     world, rank, local = dist_env()
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # TILEFFT_BENCH_BACKEND=gloo + TILEFFT_BENCH_DEVICE=0: functional check of the N>1 path with every
+        # rank on one GPU (NCCL refuses duplicate GPUs); timing such a run means nothing
+        dev_idx = int(os.environ.get("TILEFFT_BENCH_DEVICE", local))
+        torch.cuda.set_device(dev_idx)
+        backend = os.environ.get("TILEFFT_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()

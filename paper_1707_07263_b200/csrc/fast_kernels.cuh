@@ -716,55 +716,80 @@ struct FinalCfg {
   static constexpr int SMEM = (A > B ? A : B) * (int)sizeof(V);
 };
 
+// tile -> (batch, leading-digit chunk, other digits o)
+struct FinalTileGeo {
+  long long batch, chunk, o;
+};
+__device__ __forceinline__ FinalTileGeo final_geo(const FinalArgs& a, long long tile) {
+  const long long tiles_per_batch = a.chunks * a.sw0;
+  const long long rem = tile % tiles_per_batch;
+  return {tile / tiles_per_batch, rem / a.sw0, rem % a.sw0};
+}
+
+// phase 0: this thread's R elements of row (chunk*F + ff)*sw0 + o, lanes along n (coalesced loads)
+template <typename Real, int L, int F_>
+__device__ __forceinline__ void final_load(const C2<Real>* in, const FinalArgs& a, long long tile, C2<Real>* v) {
+  using Cfg = FinalCfg<Real, L, F_>;
+  using Sh = typename Cfg::Sh;
+  const FinalTileGeo g = final_geo(a, tile);
+  const int ff = threadIdx.x / Sh::T, t = threadIdx.x % Sh::T;
+  const long long grow = (g.chunk * Cfg::F + ff) * a.sw0 + g.o;
+  const C2<Real>* src = in + g.batch * a.bstride + grow * L;
+#pragma unroll
+  for (int q = 0; q < Sh::R; ++q) v[q] = src[t + q * Sh::T];
+}
+
+// phase 1: the row FFT in registers (exchange in the row's padded region), then the spectrum written
+// transposed, sm[k * TS + ff]; ends with the CTA barrier that makes it visible to phase 2
 template <typename Real, int L, bool INV, int F_>
-__device__ __forceinline__ void final_tile(const C2<Real>* in, C2<Real>* out, const FinalArgs& a,
-                                           const C2<Real>* __restrict__ tw, Real scale, long long tile, C2<Real>* sm) {
+__device__ __forceinline__ void final_fft(C2<Real>* v, const C2<Real>* __restrict__ tw, C2<Real>* sm) {
   using Cfg = FinalCfg<Real, L, F_>;
   using V = C2<Real>;
   using Sh = typename Cfg::Sh;
-  constexpr int F = Cfg::F;
-  const long long tiles_per_batch = a.chunks * a.sw0;
-  const long long batch = tile / tiles_per_batch;
-  const long long rem = tile % tiles_per_batch;
-  const long long o = rem % a.sw0, chunk = rem / a.sw0;
-  // phase 1: FFT of row (chunk*16 + ff)*sw0 + o, lanes along n
-  {
-    const int ff = threadIdx.x / Sh::T, t = threadIdx.x % Sh::T;
-    const long long grow = (chunk * F + ff) * a.sw0 + o;
-    const V* src = in + batch * a.bstride + grow * L;
-    V v[Sh::R];
+  const int ff = threadIdx.x / Sh::T, t = threadIdx.x % Sh::T;
+  V* reg = sm + ff * Cfg::REG;
+  auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
+  SyncBlock s;
+  Stages<V, L, Cfg::RMAX, INV, 0>::run(v, t, ex, tw, s);
+  __syncthreads();  // exchange regions are reused by the transpose below
 #pragma unroll
-    for (int q = 0; q < Sh::R; ++q) v[q] = src[t + q * Sh::T];
-    V* reg = sm + ff * Cfg::REG;
-    auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
-    SyncBlock s;
-    Stages<V, L, Cfg::RMAX, INV, 0>::run(v, t, ex, tw, s);
-    __syncthreads();  // exchange regions are reused by the transpose below
-#pragma unroll
-    for (int j = 0; j < Sh::R; ++j) sm[out_index<L, Cfg::RMAX>(t, j) * Cfg::TS + ff] = v[j];
-  }
+  for (int j = 0; j < Sh::R; ++j) sm[out_index<L, Cfg::RMAX>(t, j) * Cfg::TS + ff] = v[j];
   __syncthreads();
-  // phase 2: lanes along the 16 consecutive outputs
-  {
-    const int f = threadIdx.x % F, kk = threadIdx.x / F;
-    constexpr int KSTEP = Cfg::THREADS / F;
-    // out index of (d0 = chunk*16 + f, other digits from o) = d0 + final(o)
-    const long long ob = batch * a.bstride + chunk * F + f + [&] {
-      long long outi = 0, r2 = o;
-      for (int i = 0; i + 1 < a.p; ++i) {
-        const long long d = r2 / a.sub_w[i];
-        r2 -= d * a.sub_w[i];
-        outi += d * a.out_w[i];
-      }
-      return outi;
-    }();
-#pragma unroll 4
-    for (int k = kk; k < L; k += KSTEP) {
-      V x = sm[k * Cfg::TS + f];
-      if (scale != (Real)1) x = mk(x.x * scale, x.y * scale);
-      out[ob + (long long)k * a.out_w_last] = x;
-    }
+}
+
+// phase 2: lanes along the 16 consecutive outputs of each k
+template <typename Real, int L, int F_>
+__device__ __forceinline__ void final_store(C2<Real>* out, const FinalArgs& a, long long tile, const C2<Real>* sm,
+                                            Real scale) {
+  using Cfg = FinalCfg<Real, L, F_>;
+  using V = C2<Real>;
+  constexpr int F = Cfg::F;
+  const FinalTileGeo g = final_geo(a, tile);
+  const int f = threadIdx.x % F, kk = threadIdx.x / F;
+  constexpr int KSTEP = Cfg::THREADS / F;
+  // out index of (d0 = chunk*16 + f, other digits from o) = d0 + final(o)
+  long long outi = 0, r2 = g.o;
+  for (int i = 0; i + 1 < a.p; ++i) {
+    const long long d = r2 / a.sub_w[i];
+    r2 -= d * a.sub_w[i];
+    outi += d * a.out_w[i];
   }
+  const long long ob = g.batch * a.bstride + g.chunk * F + f + outi;
+#pragma unroll 4
+  for (int k = kk; k < L; k += KSTEP) {
+    V x = sm[k * Cfg::TS + f];
+    if (scale != (Real)1) x = mk(x.x * scale, x.y * scale);
+    out[ob + (long long)k * a.out_w_last] = x;
+  }
+}
+
+template <typename Real, int L, bool INV, int F_>
+__device__ __forceinline__ void final_tile(const C2<Real>* in, C2<Real>* out, const FinalArgs& a,
+                                           const C2<Real>* __restrict__ tw, Real scale, long long tile, C2<Real>* sm) {
+  C2<Real> v[FinalCfg<Real, L, F_>::Sh::R];
+  final_load<Real, L, F_>(in, a, tile, v);
+  final_fft<Real, L, INV, F_>(v, tw, sm);
+  final_store<Real, L, F_>(out, a, tile, sm, scale);
 }
 
 template <typename Real, int L, bool INV, int F_ = FOf<Real>::v>
@@ -774,6 +799,29 @@ k_final_t(const C2<Real>* in, C2<Real>* out, FinalArgs a, const C2<Real>* __rest
   final_tile<Real, L, INV, F_>(in, out, a, tw, scale, blockIdx.x, reinterpret_cast<C2<Real>*>(smem_raw));
 }
 
+// Persistent K_FINAL_T with the next tile's loads in flight during this tile's stores: once the
+// spectrum sits transposed in shared memory the row registers are free, so they take the next
+// tile's elements (plain loads, no extra shared memory) while the stores drain from shared memory.
+template <typename Real, int L, bool INV, int F_, int MINB>
+__global__ void __launch_bounds__(FinalCfg<Real, L, F_>::THREADS, MINB)
+k_final_p(const C2<Real>* in, C2<Real>* out, FinalArgs a, const C2<Real>* __restrict__ tw, Real scale) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  C2<Real>* sm = reinterpret_cast<C2<Real>*>(smem_raw);
+  long long tile = blockIdx.x;
+  if (tile >= a.ntiles) return;
+  C2<Real> v[FinalCfg<Real, L, F_>::Sh::R];
+  final_load<Real, L, F_>(in, a, tile, v);
+#pragma unroll 1
+  for (;;) {
+    final_fft<Real, L, INV, F_>(v, tw, sm);
+    const long long next = tile + gridDim.x;
+    if (next < a.ntiles) final_load<Real, L, F_>(in, a, next, v);
+    final_store<Real, L, F_>(out, a, tile, sm, scale);
+    if (next >= a.ntiles) break;
+    tile = next;
+    __syncthreads();  // the next FFT's exchange overwrites the transposed tile
+  }
+}
 
 // ------------------------------------------------------------------ K_ROWS_PF
 // Persistent K_ROWS for long fp32 rows (L = 2048..8192: one CTA per row,

@@ -262,14 +262,23 @@ int launch_final(const Pass& ps, const void* in, void* out, const void* tb, cons
       return 0;
     }
   }
-  // (a persistent TMA-prefetching variant -- 16 bulk row copies per tile, exchange
-  // and transpose in two rounds to make room for the slot -- measured slower at
-  // 2^30: 12.41 vs 11.82 ms)
+  // persistent: the next tile's row loads are in flight while this tile's transposed stores drain
+  // (measured vs one CTA per tile: 2^26 671 vs 685 us, 2^24 175 vs 181 us, 2^30 11.66 vs 12.06 ms;
+  // tools/gpu/r02_finalp.sh)
   using Cfg = tfb::FinalCfg<Real, L>;
-  auto k = tfb::k_final_t<Real, L, INV>;
+  constexpr int MINB = Cfg::THREADS <= 128 ? 4 : Cfg::THREADS <= 256 ? 2 : 1;
+  auto k = tfb::k_final_p<Real, L, INV, tfb::FOf<Real>::v, MINB>;
   if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
-  k<<<(unsigned)ps.grid, Cfg::THREADS, Cfg::SMEM, st>>>((const V*)in, (V*)out, ps.fin, (const V*)tb + ps.tw_off,
-                                                        scale);
+  static int blocks_per_sm[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& bps = blocks_per_sm[dev & 15];
+  if (!bps) {
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, Cfg::THREADS, Cfg::SMEM));
+    if (bps < 1) bps = 1;
+  }
+  const long long grid = std::max<long long>(1, std::min<long long>(ps.fin.ntiles, (long long)sm_count() * bps));
+  k<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, st>>>((const V*)in, (V*)out, ps.fin, (const V*)tb + ps.tw_off, scale);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -1426,8 +1426,12 @@ int tilefft_plan_info(tilefft_plan_t P, tilefft_plan_info_t* info) {
   info->mode = P->mode;
   info->is_2d = P->is2d;
   info->passes = (uint32_t)P->passes.size();
-  for (size_t i = 0; i < P->dev_factors.size() && i < 16; ++i) info->factors[i] = P->dev_factors[i];
   info->launches_per_exec = (uint32_t)P->passes.size();
+  if (P->is_dist) {  // pass 1 (+ the barrier kernel of tilefft_dist_exec) + the local row plan
+    info->passes = 1 + (uint32_t)(P->inner ? P->inner->passes.size() : 0);
+    info->launches_per_exec = info->passes + 1;
+  }
+  for (size_t i = 0; i < P->dev_factors.size() && i < 16; ++i) info->factors[i] = P->dev_factors[i];
   info->workspace_bytes = P->work.bytes;
   info->table_bytes = P->tables.bytes;
   return 0;

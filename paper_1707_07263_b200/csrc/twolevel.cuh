@@ -705,7 +705,21 @@ k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUten
       }
     } else {
       // ---- B: LB-point DFTs over n1 for KB k2 values of 16 combs
-      if (w == 0 && lane == 0) signal_relaxed(doneB + slot);  // scratch block is in shared memory
+      if (w == 0) {
+        // the item's scratch block is in shared memory now: drop its lines from L2 (dirty scratch is never
+        // written back to DRAM), then hand the scratch slot back
+        if (a.discard) {
+          constexpr int LPS = KB * 8 / 128;  // 128-byte lines per (n1, comb) segment of KB elements
+          const V* base = a.scratch + (size_t)slot * LB * F * LA + (size_t)sub * KB;
+#pragma unroll 4
+          for (int i = lane; i < LB * F * LPS; i += 32)
+            discard_l2(base + (size_t)(i / LPS) * LA + (i % LPS) * 16);
+          __syncwarp();
+          if (lane == 0) signal_release(doneB + slot);
+        } else if (lane == 0) {
+          signal_relaxed(doneB + slot);
+        }
+      }
       const int kb = sub;
       // pair p of this thread: OUTT=0 lanes = (8 combs x 2 k2) per half-warp; OUTT=1 lanes along k2
       auto pair = [&](int m, int& f, int& k2l) {

@@ -93,7 +93,7 @@ def test_fast_mode_fp32_within_tolerance(tf, oracle, n):
     assert err < 5e-7, err  # much tighter than the contract: accurate roots
 
 
-@pytest.mark.parametrize("n", [2, 64, 1024, 8192, 1 << 14, 1 << 16, 1 << 20])
+@pytest.mark.parametrize("n", [2, 64, 1024, 8192, 1 << 14, 1 << 16, 1 << 20, 1 << 22])
 def test_fast_mode_fp64_within_tolerance(tf, oracle, n):
     x = oracle.random_bench_signal(n, 1)
     got = tf.fft_tiled(x, tf.make_plan(n))
@@ -101,7 +101,7 @@ def test_fast_mode_fp64_within_tolerance(tf, oracle, n):
     assert err <= tol(n, np.complex128), err
 
 
-@pytest.mark.parametrize("n", [1024, 1 << 16, 1 << 20])
+@pytest.mark.parametrize("n", [1024, 1 << 16, 1 << 20, 1 << 23])
 def test_fast_mode_inverse(tf, oracle, n):
     x = oracle.random_bench_signal(n, 4).astype(np.complex64)
     got = tf.ifft_tiled(x, tf.make_plan(n))
