@@ -330,6 +330,9 @@ int launch_two_k(const Pass& ps, const void* in, void* out, const void* tb, cons
       return 0;
     };
     using TC = tfb::TwoTmaCfg<LA, LB>;
+    // plain column passes: the B items (a 16-point DFT, no inter-pass root) take the W_L roots off the
+    // A items' critical path (8192^2: 523 vs 532 us; tools/gpu/r02_twlb.sh)
+    if constexpr (!TWID && OUTT == 0) return launch(tfb::k_two_tma<LA, LB, INV, OUTT, TWID, true>, TC::THREADS, TC::SMEM);
     return launch(tfb::k_two_tma<LA, LB, INV, OUTT, TWID>, TC::THREADS, TC::SMEM);
   }
   // warp-specialised two-level kernel: one 512-thread CTA per SM (A team + B team)

@@ -516,7 +516,8 @@ __device__ __forceinline__ void two_decode(long long id, long long NA, long long
   }
 }
 
-template <int LA, int LB, bool INV, int OUTT, bool TWID>
+// TWLB: the root W_L^{n1 k2} is applied by the B items (before their LB-point DFT) instead of the A items
+template <int LA, int LB, bool INV, int OUTT, bool TWID, bool TWLB = false>
 __global__ void __launch_bounds__(TwoTmaCfg<LA, LB>::THREADS, 1)
 k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tscr, float2* __restrict__ out,
           TwoArgs a, const float2* __restrict__ tw, const float2* __restrict__ twl, const double2* __restrict__ wc,
@@ -676,7 +677,7 @@ k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUten
       if (a.diag == 1) release_slot();
       else Stages<V, LA, 32, INV, 0>::run(v, t, ex, tw, sy, 0, release_slot);
       // W_L^{n1 k2}, k2 = t + 16 i + 32 q (register 16 i + q) = W^{n1 (t + 16 i)} * W^{32 n1 q}
-      if (a.diag != 1 && sub > 0) {
+      if (!TWLB && a.diag != 1 && sub > 0) {
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const V b0 = __ldg(twl + sub * (t + 16 * i));
@@ -752,6 +753,24 @@ k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUten
         pair(m, f, k2l);
         const int k2 = kb * KB + k2l;
         V* u = v[m];
+        if constexpr (TWLB) {
+          // W_L^{n1 k2} = w^{n1}, w = W_L^{k2}: w, w^2, w^4, w^8 from the table, the other powers as
+          // products (at most three roundings each)
+          if (a.diag != 1 && k2 > 0) {
+            constexpr int Lm = LA * LB - 1;
+            V p[LB];
+            p[1] = __ldg(twl + (k2 & Lm));
+#pragma unroll
+            for (int e = 2; e < LB; e *= 2) p[e] = __ldg(twl + ((e * k2) & Lm));
+#pragma unroll
+            for (int e = 3; e < LB; ++e) {
+              const int hi = 1 << (31 - __clz(e));
+              if (e != hi) p[e] = cmul(p[hi], p[e - hi]);
+            }
+#pragma unroll
+            for (int n1 = 1; n1 < LB; ++n1) u[n1] = ctw<INV>(u[n1], p[n1]);
+          }
+        }
         if (a.diag != 1) reg_dft<LB, INV>(u);
         const long long c = ch * F + f;
         if constexpr (TWID) {
