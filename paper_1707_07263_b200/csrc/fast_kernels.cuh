@@ -91,32 +91,7 @@ struct NoHook {
 
 // TWS: the stage-root table `tw` lives in shared memory (plain loads -> LDS)
 // instead of global memory read through the read-only path (LDG.CONSTANT).
-// 32 x 32 transpose of a warp's registers through shuffles (north-star item 3 prototype): lane l, register r
-// -> lane r, register l, in five butterfly rounds; round s swaps bit s of the lane and register indices
-// (16 register pairs x 2 SHFL + selects per round).
-template <typename V>
-__device__ __forceinline__ void warp_transpose32(V* v) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int s = 0; s < 5; ++s) {
-    const int m = 1 << s;
-    const bool up = (lane & m) != 0;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      if (i & m) continue;
-      const int j = i | m;
-      V x = up ? v[i] : v[j];
-      x.x = __shfl_xor_sync(0xffffffffu, x.x, m);
-      x.y = __shfl_xor_sync(0xffffffffu, x.y, m);
-      if (up) v[i] = x;
-      else v[j] = x;
-    }
-  }
-}
-
-// SHX (L = 1024, one warp per FFT): the stage-0 -> stage-1 exchange is a warp_transpose32 instead of a
-// round trip through shared memory.
-template <typename V, int L, int RMAX, bool INV, int S, int NR = 1, bool TWS = false, bool SHX = false>
+template <typename V, int L, int RMAX, bool INV, int S, int NR = 1, bool TWS = false>
 struct Stages {
   using Sh = Shape<L, RMAX>;
   static constexpr int RS = Sh::radix(S), NS = Sh::ns(S), NB = Sh::R / RS;
@@ -144,11 +119,7 @@ struct Stages {
     }
 #pragma unroll
     for (int i = 0; i < NB; ++i) reg_dft<RS, INV>(v + i * RS);
-    if constexpr (S + 1 < Sh::NST && SHX) {
-      static_assert(L == 1024 && RMAX == 32 && S == 0 && NR == 1, "shuffle exchange: 32 x 32 only");
-      warp_transpose32(v);
-      Stages<V, L, RMAX, INV, S + 1, NR, TWS, SHX>::run(v, t, ex, tw, sync, my_round, last);
-    } else if constexpr (S + 1 < Sh::NST) {
+    if constexpr (S + 1 < Sh::NST) {
       constexpr int RS2 = Sh::radix(S + 1), NB2 = Sh::R / RS2, STR2 = L / RS2;
 #pragma unroll 1
       for (int round = 0; round < NR; ++round) {
@@ -172,7 +143,7 @@ struct Stages {
         }
         sync();
       }
-      Stages<V, L, RMAX, INV, S + 1, NR, TWS, SHX>::run(v, t, ex, tw, sync, my_round, last);
+      Stages<V, L, RMAX, INV, S + 1, NR, TWS>::run(v, t, ex, tw, sync, my_round, last);
     }
   }
 };
@@ -329,10 +300,7 @@ struct RowsTmaCfg {
   static constexpr int TW_BYTES = Sh::TW_TOTAL * (int)sizeof(V);  // stage roots staged in smem (TWS variant)
 };
 
-// VAR (north-star items 2-3 prototypes, L = 1024 fp32): bit 0 = warp-shuffle transpose instead of the
-// shared-memory exchange; bit 1 = 128-bit stores (adjacent lanes swap one value per register pair so each
-// lane owns two consecutive outputs).
-template <typename Real, int L, int WARPS, int S, bool INV, bool TWS = false, int VAR = 0>
+template <typename Real, int L, int WARPS, int S, bool INV, bool TWS = false>
 __global__ void __launch_bounds__(WARPS * 32)
 k_rows_tma(const C2<Real>* in, C2<Real>* out, long long nrows, const C2<Real>* __restrict__ tw_g, Real scale) {
   using Cfg = RowsTmaCfg<Real, L, WARPS, S>;
@@ -389,11 +357,7 @@ k_rows_tma(const C2<Real>* in, C2<Real>* out, long long nrows, const C2<Real>* _
     V v[Sh::R];
 #pragma unroll
     for (int q = 0; q < Sh::R; ++q) v[q] = reg[tt + q * Sh::T];
-    if constexpr (Cfg::EXCH && (VAR & 1)) {
-      auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
-      SyncWarp sy;
-      Stages<V, L, Cfg::RMAX, INV, 0, 1, TWS, true>::run(v, tt, ex, tw, sy);
-    } else if constexpr (Cfg::EXCH) {
+    if constexpr (Cfg::EXCH) {
       __syncwarp();
       auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
       SyncWarp sy;
@@ -404,27 +368,7 @@ k_rows_tma(const C2<Real>* in, C2<Real>* out, long long nrows, const C2<Real>* _
       Stages<V, L, Cfg::RMAX, INV, 0, 1, TWS>::run(v, tt, ex, tw, sy);
     }
     const long long row = c * FPW + ff;
-    if constexpr (VAR & 2) {
-      static_assert(L == 1024 && std::is_same<Real, float>::value, "128-bit stores: fp32 L = 1024");
-      // lane t holds X[t + 32 q]; for each register pair (q, q+1) the even lane takes X[32q + t + 1] from
-      // its odd neighbour and stores (X[32q+t], X[32q+t+1]); the odd lane takes X[32(q+1) + t - 1]
-      const bool odd = lane & 1;
-      float4* dst4 = reinterpret_cast<float4*>(out + row * L);
-#pragma unroll
-      for (int q = 0; q < 32; q += 2) {
-        V send = odd ? v[q] : v[q + 1];
-        V got;
-        got.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
-        got.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
-        V lo = odd ? got : v[q], hi = odd ? v[q + 1] : got;
-        if (scale != (Real)1) {
-          lo = mk(lo.x * scale, lo.y * scale);
-          hi = mk(hi.x * scale, hi.y * scale);
-        }
-        const int e = odd ? 32 * (q + 1) + lane - 1 : 32 * q + lane;  // even element index of the pair
-        if (row < nrows) dst4[e >> 1] = make_float4(lo.x, lo.y, hi.x, hi.y);
-      }
-    } else if (row < nrows) {
+    if (row < nrows) {
       V* dst = out + row * L;
 #pragma unroll
       for (int j = 0; j < Sh::R; ++j) {

@@ -43,10 +43,10 @@ constexpr int kRowsWarps = 4;
 constexpr int kRowsStages = 2;
 
 // one persistent TMA rows launch with W warps per CTA and an S-deep ring per warp
-template <typename Real, int L, bool INV, int W, int S, int VAR = 0>
+template <typename Real, int L, bool INV, int W, int S>
 int launch_rows_tma(const Pass& ps, const void* in, void* out, const void* tw, Real scale, cudaStream_t st) {
   using Cfg = tfb::RowsTmaCfg<Real, L, W, S>;
-  auto k = tfb::k_rows_tma<Real, L, W, S, INV, false, VAR>;
+  auto k = tfb::k_rows_tma<Real, L, W, S, INV>;
   const int smem = Cfg::SMEM;
   if (int rc = ensure_smem((const void*)k, smem)) return rc;
   static int blocks_per_sm[16] = {};
@@ -75,13 +75,6 @@ int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, const
     if (aligned && !ps.no_tma) {
       // stage roots through the read-only path, not shared memory (measured:
       // profiles/r02_twiddle_ab.txt, tools/microbench/twiddle_ab.cu);
-      if constexpr (std::is_same<Real, float>::value && L == 1024) {
-        // north-star prototypes (measured): 1 = shuffle exchange, 2 = 128-bit stores, 3 = both
-        static const int var = env_int_or("TILEFFT_ROWS_VAR", 0);
-        if (var == 1) return launch_rows_tma<Real, L, INV, kRowsWarps, kRowsStages, 1>(ps, in, out, tw, scale, st);
-        if (var == 2) return launch_rows_tma<Real, L, INV, kRowsWarps, kRowsStages, 2>(ps, in, out, tw, scale, st);
-        if (var == 3) return launch_rows_tma<Real, L, INV, kRowsWarps, kRowsStages, 3>(ps, in, out, tw, scale, st);
-      }
       return launch_rows_tma<Real, L, INV, kRowsWarps, kRowsStages>(ps, in, out, tw, scale, st);
     }
   }
