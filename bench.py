@@ -44,6 +44,8 @@ CONFIGS = {
     "1d_2e26": (1 << 26, 1, "1d", 2, "single 1D complex fp32 forward FFT N=2^26 (BASELINE configs[2])"),
     "2d_8192": (8192, 1, "2d", 2, "2D complex fp32 forward FFT 8192x8192, one image per GPU (BASELINE configs[3])"),
     "1d_2e30": (1 << 30, 1, "1d", 3, "single 1D complex fp32 forward FFT N=2^30 on one GPU (BASELINE configs[4])"),
+    "1d_2e30_natural": (1 << 30, 1, "1d", 3, "distributed 1D complex fp32 forward FFT N=2^30 with natural-order "
+                        "block I/O (SURVEY 8e option: one all-to-all before and one after the four-step exchange)"),
 }
 
 
@@ -54,6 +56,7 @@ DEVICE_FACTORS = {
     "1d_2e26": [512, 512, 256],
     "2d_8192": [8192, 8192],
     "1d_2e30": [1024, 1024, 1024],
+    "1d_2e30_natural": [1024, 1024, 1024],
 }
 
 
@@ -372,14 +375,20 @@ def bench_config(name, args, torch, dev, world, rank, steps, warmup, with_cpu, w
         dfft = DistributedFFT(total, exchange=args.exchange, device=dev)
         o = dfft.ops
         elems = o.n1 * o.c
+        natural = name.endswith("_natural")
         x = device_input(torch, elems, 1 + rank, dev).view(torch.complex64).view(o.n1, o.c)
         y = o.alloc((o.r, o.n2))
+        if natural:  # this rank's contiguous 1/G of the signal in, its contiguous 1/G of the spectrum out
+            x = x.reshape(-1)
         fac = o.plan.info()["factors"]  # [N1] + the local row plan's passes
         info = {"passes": len(fac), "factors": fac,
                 "launches_per_exec": len(fac) + (1 if getattr(dfft, "device_barrier", False) else 0)}
 
         def step():
-            dfft.forward(x, y)
+            if natural:
+                dfft.forward_natural(x)
+            else:
+                dfft.forward(x, y)
     else:
         plan = make_device_plan(name, dev)
         info = plan.info()
@@ -440,7 +449,7 @@ def bench_config(name, args, torch, dev, world, rank, steps, warmup, with_cpu, w
         torch.cuda.synchronize()
         a.record(stream)
         for _ in range(reps):
-            o.pass1(x, _capi.FORWARD)
+            o.pass1(x.view(o.n1, o.c), _capi.FORWARD)
         b.record(stream)
         torch.cuda.synchronize()
         p1_ms = max_over_ranks(torch, dist, a.elapsed_time(b) / reps, dev)
@@ -512,6 +521,7 @@ def bench_config(name, args, torch, dev, world, rank, steps, warmup, with_cpu, w
     rec = {"value": round(value, 2), "unit": "GFLOP/s", "ms_per_step": round(ms_step, 5), "steps": steps,
            "warmup": warmup, "scaling": "strong" if distributed else "weak", "config": config_key(name),
            "parallelism": (f"four-step over {world} GPUs, {args.exchange} all-to-all fused into pass 1"
+                           + (", natural-order block I/O (+2 NCCL all-to-alls)" if name.endswith("_natural") else "")
                            if distributed else f"batch sharded over {world} GPU(s), no collective"),
            "device_factors": info["factors"], "hbm_gbs": round(step_bytes / (ms_step * 1e-3) / 1e9, 1),
            "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "cufft": cufft, "nvlink": nvlink,
@@ -574,7 +584,7 @@ def main():
     if args.configs is None:
         subs = ([c for c in ("1d_2e20", "1d_2e26", "2d_8192", "1d_2e30") if c != args.config]
                 if args.config == "batched1024" and world == 1 else
-                (["2d_8192", "1d_2e30"] if args.config == "batched1024" else []))
+                (["2d_8192", "1d_2e30", "1d_2e30_natural"] if args.config == "batched1024" else []))
     else:
         subs = [] if args.configs == "none" else [c for c in args.configs.split(",") if c and c != args.config]
     with_cpu = not args.no_cpu_baseline

@@ -55,6 +55,12 @@ def column_slab(x: np.ndarray, world: int, rank: int) -> np.ndarray:
     return np.ascontiguousarray(x.reshape(n1, n2)[:, rank * c:(rank + 1) * c])
 
 
+def natural_block(x: np.ndarray, world: int, rank: int) -> np.ndarray:
+    """Rank `rank`'s contiguous 1/world of a natural-order array (forward_natural's I/O layout)."""
+    m = x.shape[-1] // world
+    return np.ascontiguousarray(x[rank * m:(rank + 1) * m])
+
+
 def assemble_output(slabs, n: int) -> np.ndarray:
     """Natural-order spectrum from every rank's row slab [R][N2]."""
     world = len(slabs)
@@ -198,6 +204,30 @@ class DistributedFFT:
             self.rows.view(o.r, self.world, o.c).copy_(self.recv.permute(1, 0, 2))
         o.pass2(self.rows, out, sign)
         return out
+
+    def forward_natural(self, x_block, inverse: bool = False):
+        """Natural-order block I/O (SURVEY §8e option): x_block is this rank's contiguous 1/G of the signal,
+        x[g·N/G : (g+1)·N/G]; returns this rank's contiguous 1/G of the spectrum, X[g·N/G : (g+1)·N/G].
+
+        Costs one all-to-all before the four-step exchange (rows n1 ∈ [gR, (g+1)R) of the [N1][N2] signal
+        matrix -> the column slab) and one after it (the digit-interleaved row slab -> natural blocks), each
+        an ``all_to_all_single`` plus one strided copy; the in-kernel exchange of pass 1 is unchanged."""
+        o = self.ops
+        G, R, C, N1, N2 = self.world, o.r, o.c, o.n1, o.n2
+        M = N2 // G
+        if G == 1:
+            return self.forward(x_block.reshape(N1, N2), inverse=inverse).reshape(-1)
+        # 1. block rows [R][N2] -> per-destination column blocks [G][R][C] -> column slab [N1][C]
+        send = x_block.reshape(R, G, C).permute(1, 0, 2).contiguous()
+        col = o.alloc((G, R, C))
+        self.dist.all_to_all_single(col, send)
+        y = self.forward(col.reshape(N1, C), inverse=inverse)  # row slab [R][N2]: X[(gR + k1) + N1 k2]
+        # 2. rows k1 of this rank, spectrum columns k2 of each destination's natural block -> [G][R][M]
+        send2 = y.reshape(R, G, M).permute(1, 0, 2).contiguous()
+        recv2 = o.alloc((G, R, M))
+        self.dist.all_to_all_single(recv2, send2)
+        # recv2[s][k1 - sR][m] = X[k1 + N1 (gM + m)]: natural order is m-major, k1-minor
+        return recv2.reshape(N1, M).t().contiguous().reshape(-1)
 
     def close(self):
         for p in self._opened:

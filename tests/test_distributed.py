@@ -196,6 +196,56 @@ def test_distributed_four_step_orchestration_gloo():
     assert shares == [(0, 5), (5, 10)]
 
 
+def _natural_worker(rank, world, port, n, exchange, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, os.path.dirname(HERE))
+    from paper_1707_07263_b200.distributed import DistributedFFT, natural_block
+    sys.path.insert(0, HERE)
+    from oracle_lib import Oracle
+    O = Oracle()
+    ops = SharedMemOracleOps(n, world, rank) if exchange == "p2p" else OracleOps(n, world, rank)
+    d = DistributedFFT(n, exchange=exchange, ops=ops)
+    outs = []
+    for seed in (21, 22):
+        x = O.random_bench_signal(n, seed)
+        outs.append(d.forward_natural(torch.from_numpy(natural_block(x, world, rank))).numpy().copy())
+    gathered = [None] * world
+    dist.all_gather_object(gathered, outs)
+    if rank == 0:
+        q.put(gathered)
+    dist.barrier()
+    for path in getattr(ops, "paths", []):
+        os.unlink(path)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
+def test_distributed_natural_order_io_gloo(exchange):
+    """Natural-order block I/O (SURVEY §8e option): each rank passes its contiguous 1/G of x and gets its
+    contiguous 1/G of X; the concatenation equals the oracle's transform."""
+    import multiprocessing as mp
+    sys.path.insert(0, HERE)
+    from oracle_lib import Oracle, rel_l2
+    n, world = 1 << 16, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_natural_worker, args=(r, world, port, n, exchange, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    gathered = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    O = Oracle()
+    for call, seed in enumerate((21, 22)):
+        got = np.concatenate([gathered[r][call] for r in range(world)])
+        assert rel_l2(got, O.fft_tiled(O.random_bench_signal(n, seed))) < 1e-12, call
+
+
 def test_layout_helpers_roundtrip():
     from paper_1707_07263_b200.distributed import column_slab, four_step_layout, shard_rows
     n, world = 1 << 18, 4
