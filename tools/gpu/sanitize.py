@@ -1,6 +1,7 @@
-"""Small transforms through the kernels added this round, for compute-sanitizer
-(memcheck / racecheck / synccheck): two-level passes (k_two_ws, both output
-layouts, inverse), the prefetching long-row kernel, the fused small kernel."""
+"""Small transforms through the round-2 kernels, for compute-sanitizer (memcheck / racecheck /
+synccheck): the two-level pass k_two_tma (plain columns with B-side roots, both output layouts of the
+four-step 1D plan, inverse), the persistent final pass k_final_p, the prefetching long-row kernel.
+(The distributed barrier kernel waits for kernels on other streams, which the sanitizer serialises.)"""
 import os, sys
 import numpy as np
 sys.path.insert(0, os.getcwd())
@@ -37,6 +38,6 @@ run2d(2048, 32)
 run2d(2048, 32, _capi.INVERSE)
 run2d(256, 2048)
 run1d(1 << 22, {"TILEFFT_TWO_1D": "1"})
-run1d(1 << 16, {"TILEFFT_FUSE": "1"})
+run1d(1 << 22, {})
 run1d(8192, {})
 print("sanitize workload ok")
