@@ -81,7 +81,8 @@ int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, const
   if constexpr (std::is_same<Real, float>::value && L >= 2048) {
     if (aligned && !ps.no_tma) {
       using CfgP = tfb::RowsPfCfg<L>;
-      auto k = tfb::k_rows_pf<L, INV>;
+      static const int pf3 = env_int_or("TILEFFT_ROWS_PF3", 0);  // experiment: 3 CTAs per SM (register cap)
+      auto k = pf3 ? tfb::k_rows_pf<L, INV, 3> : tfb::k_rows_pf<L, INV>;
       if (int rc = ensure_smem((const void*)k, CfgP::SMEM)) return rc;
       int bps = 0;
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, CfgP::THREADS, CfgP::SMEM));
