@@ -838,8 +838,8 @@ struct RowsPfCfg {
   static constexpr int SMEM = REG * 8 + 16;
 };
 
-template <int L, bool INV, int MINB = 2>
-__global__ void __launch_bounds__(RowsPfCfg<L>::THREADS, MINB)
+template <int L, bool INV>
+__global__ void __launch_bounds__(RowsPfCfg<L>::THREADS, 2)
 k_rows_pf(const float2* __restrict__ in, float2* __restrict__ out, long long nrows, const float2* __restrict__ tw,
           float scale) {
   using Cfg = RowsPfCfg<L>;

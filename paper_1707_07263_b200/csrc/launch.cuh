@@ -81,8 +81,8 @@ int launch_rows(const Pass& ps, const void* in, void* out, const void* tw, const
   if constexpr (std::is_same<Real, float>::value && L >= 2048) {
     if (aligned && !ps.no_tma) {
       using CfgP = tfb::RowsPfCfg<L>;
-      static const int pf3 = env_int_or("TILEFFT_ROWS_PF3", 0);  // experiment: 3 CTAs per SM (register cap)
-      auto k = pf3 ? tfb::k_rows_pf<L, INV, 3> : tfb::k_rows_pf<L, INV>;
+      // (3 CTAs per SM -- register cap 80, 316 bytes of spills -- measured 604 vs 519 us for 8192^2)
+      auto k = tfb::k_rows_pf<L, INV>;
       if (int rc = ensure_smem((const void*)k, CfgP::SMEM)) return rc;
       int bps = 0;
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, CfgP::THREADS, CfgP::SMEM));
@@ -333,7 +333,12 @@ int launch_two_k(const Pass& ps, const void* in, void* out, const void* tb, cons
     using TC = tfb::TwoTmaCfg<LA, LB>;
     // plain column passes: the B items (a 16-point DFT, no inter-pass root) take the W_L roots off the
     // A items' critical path (8192^2: 523 vs 532 us; tools/gpu/r02_twlb.sh)
-    if constexpr (!TWID && OUTT == 0) return launch(tfb::k_two_tma<LA, LB, INV, OUTT, TWID, true>, TC::THREADS, TC::SMEM);
+    // 19 compute warps at <= 96 registers (16 at 128 before): 8192^2 columns 503 vs 519 us; 23 warps
+    // (80 registers, spills) 535 us (tools/gpu/r02_cw.sh)
+    if constexpr (!TWID && OUTT == 0) {
+      using TCB = tfb::TwoTmaCfg<LA, LB, 19>;
+      return launch(tfb::k_two_tma<LA, LB, INV, OUTT, TWID, true, TCB::CW>, TCB::THREADS, TCB::SMEM);
+    }
     return launch(tfb::k_two_tma<LA, LB, INV, OUTT, TWID>, TC::THREADS, TC::SMEM);
   }
   // warp-specialised two-level kernel: one 512-thread CTA per SM (A team + B team)

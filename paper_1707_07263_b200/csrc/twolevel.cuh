@@ -457,7 +457,7 @@ k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, Two
 // deferred to just before the warp's next global stores (by then the stores
 // it orders have drained), or earlier if the warp would otherwise block on a
 // slot -- so a warp never waits on a release another CTA may need.
-template <int LA, int LB>
+template <int LA, int LB, int CW_ = 15>
 struct TwoTmaCfg {
   static constexpr int F = 16;
   static constexpr int L = LA * LB;
@@ -465,7 +465,8 @@ struct TwoTmaCfg {
   static constexpr int SLOT = LA * F;             // elements per item (A tile == B block)
   static constexpr int SLOT_BYTES = SLOT * 8;     // 64 KB
   static constexpr int S = 3;                     // slots
-  static constexpr int CW = 15;                   // compute warps (16 warps: 128 registers each)
+  static constexpr int CW = CW_;                  // compute warps (15: 128 registers; 19: <= 96 registers)
+  static constexpr int NTERM = (CW + 7) / 8;      // terminal items: one unit for every compute warp
   static constexpr int THREADS = 32 * (1 + CW);
   static constexpr int PAIRS = KB * F / 256;      // B (comb, k2) pairs per compute thread
   static constexpr int SMEM = S * SLOT_BYTES + 2 * S * 8 + 1024;
@@ -517,12 +518,14 @@ __device__ __forceinline__ void two_decode(long long id, long long NA, long long
 }
 
 // TWLB: the root W_L^{n1 k2} is applied by the B items (before their LB-point DFT) instead of the A items
-template <int LA, int LB, bool INV, int OUTT, bool TWID, bool TWLB = false>
-__global__ void __launch_bounds__(TwoTmaCfg<LA, LB>::THREADS, 1)
+// CW: compute warps. 19 (at most 96 registers) for the plain column pass, which fits them without spills;
+// the variants carrying the inter-pass root keep 15 (128 registers)
+template <int LA, int LB, bool INV, int OUTT, bool TWID, bool TWLB = false, int CW = (TWLB ? 19 : 15)>
+__global__ void __launch_bounds__(TwoTmaCfg<LA, LB, CW>::THREADS, 1)
 k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tscr, float2* __restrict__ out,
           TwoArgs a, const float2* __restrict__ tw, const float2* __restrict__ twl, const double2* __restrict__ wc,
           const double2* __restrict__ wf, float scale) {
-  using Cfg = TwoTmaCfg<LA, LB>;
+  using Cfg = TwoTmaCfg<LA, LB, CW>;
   using V = float2;
   constexpr int F = Cfg::F, S = Cfg::S, KB = Cfg::KB;
   extern __shared__ unsigned char smem_raw[];
@@ -613,9 +616,9 @@ k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUten
             tma_load_4d_l2(dst + h * LB * 16 * 16, &tscr, sub * KB + 16 * h, 0, 0, slot, &full[s]);
         }
       }
-      // end of work: terminal items k and k + 1 (the compute warps hold at most 15 units)
+      // end of work: NTERM terminal items, one unit for every compute warp
 #pragma unroll 1
-      for (int j = 0; j < 2; ++j, ++k) {
+      for (int j = 0; j < Cfg::NTERM; ++j, ++k) {
         const int s = k % S;
         if (k >= S) mbar_wait(&empty[s], (uint32_t)(((k / S) - 1) & 1));
         s_id[s] = -1;
@@ -628,8 +631,8 @@ k_two_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUten
 
   // ============================================================== compute
   // Each item is 8 units (A: combs 2p, 2p+1; B: 1/8 of the pairs); compute warps take units in
-  // order from a shared counter, so any number of warps (up to 16) shares the items. At most 15
-  // units are outstanding, i.e. a warp is never two slot phases ahead of the loader.
+  // order from a shared counter, so any number of warps shares the items; a warp that runs ahead
+  // of a slot's in-flight TMA waits on the slot's sequence tag first (s_seq), never on a wrong phase.
 #pragma unroll 1
   for (;;) {
     unsigned u = 0;
