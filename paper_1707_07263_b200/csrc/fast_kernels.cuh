@@ -518,7 +518,7 @@ k_comb(const C2<Real>* in, C2<Real>* out, CombArgs a, const C2<Real>* __restrict
 // released as soon as its inputs are in registers, so the next tile's load
 // overlaps the butterflies, the exchange (a separate buffer, in NR rounds
 // when the tile is larger than it) and the stores.
-template <typename Real, int L, int F_ = FOf<Real>::v>
+template <typename Real, int L, int F_ = FOf<Real>::v, bool IP_ = false>
 struct CombTmaCfg {
   using V = C2<Real>;
   static constexpr int RMAX = RmaxOf<Real>::v;
@@ -527,14 +527,18 @@ struct CombTmaCfg {
   static constexpr int THREADS = F * Sh::T;
   static constexpr int TILE = L * F;                       // elements
   static constexpr int TILE_BYTES = TILE * (int)sizeof(V);
-  // One slot per CTA (released as soon as the tile is in registers, so the
-  // next tile streams in during the butterflies) plus a half-tile exchange
-  // buffer used in two rounds: 1.5 tiles of shared memory, which lets >= 16
-  // warps per SM stay resident (2 CTAs of 8 warps at L = 512, ...).
+  // One slot per CTA. Default (IP, the product): the Stockham exchange runs
+  // in place in the slot in one round and the next tile is issued once the
+  // exchange has been read back. Otherwise: the slot is released as soon as
+  // the tile is in registers and a half-tile exchange buffer is used in two
+  // rounds (1.5 tiles of shared memory) -- measured 7-12 % slower.
+  // IP: the exchange runs in place in the tile slot (one round, no separate buffer) and the next
+  // tile's TMA is issued once the exchange has been read back (start of the last stage)
+  static constexpr bool IP = IP_;
   static constexpr int S = 1;
-  static constexpr int NR = Sh::NST > 1 ? 2 : 1;
+  static constexpr int NR = (Sh::NST > 1 && !IP) ? 2 : 1;
   static constexpr int FX = F / NR;                        // FFTs per exchange round
-  static constexpr int XB = Sh::NST > 1 ? L * FX : 0;      // exchange elements
+  static constexpr int XB = (Sh::NST > 1 && !IP) ? L * FX : 0;  // exchange elements
   static constexpr int BL = L < 256 ? L : 256;             // TMA box rows
   static constexpr int DATA_BYTES = S * TILE_BYTES + XB * (int)sizeof(V);
   static constexpr int SMEM = DATA_BYTES + S * 8 + 128;    // + mbarriers + alignment slack
@@ -571,17 +575,17 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-template <typename Real, int L, bool INV, bool TWID, int MODE, int F_ = FOf<Real>::v>
-__global__ void __launch_bounds__(CombTmaCfg<Real, L, F_>::THREADS, CombTmaCfg<Real, L, F_>::MINB)
+template <typename Real, int L, bool INV, bool TWID, int MODE, int F_ = FOf<Real>::v, bool IP = false>
+__global__ void __launch_bounds__(CombTmaCfg<Real, L, F_, IP>::THREADS, CombTmaCfg<Real, L, F_, IP>::MINB)
 k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs a, const C2<Real>* __restrict__ tw,
            const double2* __restrict__ wc, const double2* __restrict__ wf, Real scale) {
-  using Cfg = CombTmaCfg<Real, L, F_>;
+  using Cfg = CombTmaCfg<Real, L, F_, IP>;
   using V = C2<Real>;
   using Sh = typename Cfg::Sh;
   constexpr int F = Cfg::F, S = Cfg::S;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   V* slots = reinterpret_cast<V*>(smem_raw);
-  V* xb = slots + S * Cfg::TILE;
+  V* xb = IP ? slots : slots + S * Cfg::TILE;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + Cfg::DATA_BYTES);
   const int f = threadIdx.x % F, t = threadIdx.x / F;
   const int my_round = f / Cfg::FX, fx = f % Cfg::FX;
@@ -626,9 +630,13 @@ k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs 
     V v[Sh::R];
 #pragma unroll
     for (int q = 0; q < Sh::R; ++q) v[q] = sl[(t + q * Sh::T) * F + f];
-    fence_proxy_async_smem();
-    __syncthreads();  // slot s fully consumed: refill it
-    if (threadIdx.x == 0 && tile + S * G < a.ntiles) issue(tile + S * G, s);
+    auto refill = [&]() {
+      fence_proxy_async_smem();
+      __syncthreads();  // slot s fully consumed: refill it
+      if (threadIdx.x == 0 && tile + S * G < a.ntiles) issue(tile + S * G, s);
+    };
+    if constexpr (!IP) refill();
+    else __syncthreads();  // every thread has its elements before the in-place exchange overwrites them
     // geometry of this tile (same decomposition as K_COMB)
     const long long chunk = tile % a.chunks, g = tile / a.chunks;
     const long long batch = g / a.groups_per_batch, u = g % a.groups_per_batch;
@@ -661,8 +669,11 @@ k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs 
     }
     auto ex = [xb, fx](int i) -> V& { return xb[i * Cfg::FX + fx]; };
     SyncBlock sy;
+    if constexpr (IP)
+      if (a.copy_only == 1) refill();
     if (a.copy_only != 1) {
-      Stages<V, L, Cfg::RMAX, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
+      if constexpr (IP) Stages<V, L, Cfg::RMAX, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round, refill);
+      else Stages<V, L, Cfg::RMAX, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
       if constexpr (TWID)
         if (a.copy_only != 2) interpass_scale<V, L, Cfg::RMAX, INV>(v, t, r, a.m_mask, a.fb, wc, wf);
     }

@@ -157,10 +157,10 @@ bool encode_comb_map(CUtensorMap* map, const Pass& ps, const void* in) {
 }
 
 // Persistent TMA-pipelined comb pass (K_COMB_TMA) with F-comb tiles.
-template <typename Real, int L, bool INV, int F>
+template <typename Real, int L, bool INV, int F, bool IP = false>
 int launch_comb_tma(const Pass& ps, const CUtensorMap& map, void* out, const void* tb, const void* tb64, Real scale,
                     cudaStream_t st) {
-  using Cfg = tfb::CombTmaCfg<Real, L, F>;
+  using Cfg = tfb::CombTmaCfg<Real, L, F, IP>;
   using V = tfb::C2<Real>;
   const tfb::CombArgs& c = ps.comb;
   constexpr int K = tfb::FOf<Real>::v / F;  // tiles per plan tile (the plan counts FOf-comb tiles)
@@ -183,7 +183,7 @@ int launch_comb_tma(const Pass& ps, const CUtensorMap& map, void* out, const voi
     a.out_w[i] = c.out_w[i];
     a.sub_w[i] = c.sub_w[i];
   }
-  auto k = tfb::k_comb_tma<Real, L, INV, true, 0, F>;
+  auto k = tfb::k_comb_tma<Real, L, INV, true, 0, F, IP>;
   if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
   int bps = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, Cfg::THREADS, Cfg::SMEM));
@@ -229,8 +229,14 @@ int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, const
     // (8-comb tiles -- 64-byte rows, half the shared memory -- measured 15.8 vs
     // 11.9 ms at 2^30: the 128-byte line per comb step is what keeps the
     // strided TMA reads at full DRAM efficiency)
-    if (!ps.no_tma && ps.kind == K_COMB1D && encode_comb_map<Real, L>(&map, ps, in))
+    if (!ps.no_tma && ps.kind == K_COMB1D && encode_comb_map<Real, L>(&map, ps, in)) {
+      // exchange in place in the tile slot in one round (no separate half-tile buffer used in two rounds,
+      // half the CTA barriers), next tile issued once the exchange is read back: 2^26 591 vs 670 us,
+      // 2^24 152 vs 174 us, 2^30 10.60 vs 11.40 ms (tools/gpu/r02_ip.sh, r02_ip2.sh)
+      if constexpr (tfb::Shape<L, tfb::RmaxOf<Real>::v>::NST > 1)
+        return launch_comb_tma<Real, L, INV, tfb::FOf<Real>::v, true>(ps, map, out, tb, tb64, scale, st);
       return launch_comb_tma<Real, L, INV, tfb::FOf<Real>::v>(ps, map, out, tb, tb64, scale, st);
+    }
   }
   using Cfg = tfb::CombCfg<Real, L>;
   auto go = [&](auto k) -> int {
@@ -418,7 +424,8 @@ template <typename Real, int L, bool INV>
 int launch_dist_pass1_L(const DistPass1& d, const void* in, const void* tb, const void* tb64, Real scale,
                         cudaStream_t st) {
   using V = tfb::C2<Real>;
-  using Cfg = tfb::CombTmaCfg<Real, L>;
+  constexpr bool IP = tfb::Shape<L, tfb::RmaxOf<Real>::v>::NST > 1;  // in-place exchange, as launch_comb
+  using Cfg = tfb::CombTmaCfg<Real, L, tfb::FOf<Real>::v, IP>;
   constexpr int W = (int)sizeof(V) / 8;
   auto enc = tensor_map_encoder();
   if (!enc) return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled unavailable");
@@ -433,7 +440,7 @@ int launch_dist_pass1_L(const DistPass1& d, const void* in, const void* tb, cons
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled failed for the distributed slab");
-  auto k = tfb::k_comb_tma<Real, L, INV, true, 2>;
+  auto k = tfb::k_comb_tma<Real, L, INV, true, 2, tfb::FOf<Real>::v, IP>;
   if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
   int bps = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, Cfg::THREADS, Cfg::SMEM));
