@@ -413,23 +413,24 @@ def test_distributed_step_graph_capture_virtual_ranks(oracle):
     assert rel_l2(got, oracle.fft_tiled(x)) < 5e-7
 
 
-def _ipc_worker(rank, world, port, n, q):
+def _ipc_worker(rank, world, port, n, q, per_rank_gpu=False):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(0)
+    dev = rank if per_rank_gpu else 0
+    torch.cuda.set_device(dev)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     sys.path.insert(0, os.path.dirname(HERE))
     from paper_1707_07263_b200.distributed import DistributedFFT, column_slab
     sys.path.insert(0, HERE)
     from oracle_lib import Oracle
     O = Oracle()
-    d = DistributedFFT(n, exchange="p2p", device=0)
+    d = DistributedFFT(n, exchange="p2p", device=dev)
     assert d.device_barrier
     outs = []
     for seed in (41, 42, 43):  # both slabs of the double buffer, then the first again
         x = O.random_bench_signal(n, seed).astype(np.complex64)
-        y = d.forward(torch.from_numpy(column_slab(x, world, rank)).cuda())
+        y = d.forward(torch.from_numpy(column_slab(x, world, rank)).to(f"cuda:{dev}"))
         torch.cuda.synchronize()
         outs.append(y.cpu().numpy())
     gathered = [None] * world
@@ -442,18 +443,22 @@ def _ipc_worker(rank, world, port, n, q):
 
 
 @pytest.mark.gpu
-def test_distributed_two_processes_cuda_ipc(oracle):
+@pytest.mark.parametrize("per_rank_gpu", [False, True], ids=["same_gpu", "gpu_per_rank"])
+def test_distributed_two_processes_cuda_ipc(oracle, per_rank_gpu):
     """Two real processes (gloo for the handle exchange, both on cuda:0): pass-1 stores land in the other process's
     row slab through CUDA IPC and the device flag barrier orders them — the cross-process path of the p2p exchange
     (on an 8-GPU box the same code maps peer GPUs' memory over NVLink)."""
     import multiprocessing as mp
     from paper_1707_07263_b200.distributed import assemble_output
     from oracle_lib import rel_l2
+    import torch
+    if per_rank_gpu and torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs (peer memory over NVLink); the same-GPU case covers the protocol")
     n, world = 1 << 20, 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, n, q)) for r in range(world)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, n, q, per_rank_gpu)) for r in range(world)]
     for p in procs:
         p.start()
     gathered = q.get(timeout=600)
