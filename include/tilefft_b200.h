@@ -145,6 +145,11 @@ TILEFFT_API int tilefft_dist_set_peers(tilefft_plan_t plan, void* const* dest, u
 TILEFFT_API int tilefft_dist_exec_pass1(tilefft_plan_t plan, const void* d_col_slab, int sign, void* cuda_stream);
 TILEFFT_API int tilefft_dist_exec_pass2(tilefft_plan_t plan, const void* d_row_slab, void* d_out, int sign,
                                         void* cuda_stream);
+/* Pass 2 straight from an all-to-all's receive buffer laid out [src][rows_per_rank][cols_per_rank] (source
+ * rank src's block of this rank's rows; the NCCL exchange): the row plan's first pass reads it through a
+ * 5-D tensor map, so no re-assembly copy. TILEFFT_EINVAL when the row plan is a single pass. */
+TILEFFT_API int tilefft_dist_exec_pass2_blocks(tilefft_plan_t plan, const void* d_recv, void* d_out, int sign,
+                                               void* cuda_stream);
 /* Device-side barrier for the distributed step. Each distributed plan owns a
  * small device flag buffer; export it to the other ranks (tilefft_ipc_get_handle
  * on the pointer tilefft_dist_flag_buffer returns), then give every plan all

@@ -64,6 +64,7 @@ EXPORTS = (
     "tilefft_dist_set_peers",
     "tilefft_dist_exec_pass1",
     "tilefft_dist_exec_pass2",
+    "tilefft_dist_exec_pass2_blocks",
     "tilefft_dist_flag_buffer",
     "tilefft_dist_set_flags",
     "tilefft_dist_exec",
@@ -115,6 +116,7 @@ def load() -> ctypes.CDLL:
         lib.tilefft_dist_exec_pass1.argtypes = [vp, vp, i32, vp]
         lib.tilefft_dist_exec_pass2.argtypes = [vp, vp, vp, i32, vp]
         lib.tilefft_ipc_get_handle.argtypes = [vp, vp, ctypes.POINTER(u64)]
+        lib.tilefft_dist_exec_pass2_blocks.argtypes = [vp, vp, vp, i32, vp]
         lib.tilefft_dist_flag_buffer.argtypes = [vp, ctypes.POINTER(vp)]
         lib.tilefft_dist_set_flags.argtypes = [vp, ctypes.POINTER(vp), u32]
         lib.tilefft_dist_exec.argtypes = [vp, vp, vp, i32, vp]
@@ -128,6 +130,7 @@ def load() -> ctypes.CDLL:
                      "tilefft_exchange",
                      "tilefft_interstage_scale", "tilefft_dist_plan_create", "tilefft_dist_layout",
                      "tilefft_dist_set_peers", "tilefft_dist_exec_pass1", "tilefft_dist_exec_pass2",
+                     "tilefft_dist_exec_pass2_blocks",
                      "tilefft_dist_flag_buffer", "tilefft_dist_set_flags", "tilefft_dist_exec",
                      "tilefft_ipc_get_handle", "tilefft_ipc_open_handle", "tilefft_ipc_close_handle"):
             getattr(lib, name).restype = ctypes.c_int
@@ -265,6 +268,11 @@ class DistPlan(DevicePlan):
     def pass2(self, d_rows, d_out, sign=FORWARD, stream=0):
         check(self._lib.tilefft_dist_exec_pass2(self._h, ctypes.c_void_p(d_rows), ctypes.c_void_p(d_out), int(sign),
                                                 ctypes.c_void_p(stream)))
+
+    def pass2_blocks(self, d_recv, d_out, sign=FORWARD, stream=0):
+        """pass 2 reading the all-to-all receive buffer [src][rows][cols] directly (tilefft_dist_exec_pass2_blocks)."""
+        check(self._lib.tilefft_dist_exec_pass2_blocks(self._h, ctypes.c_void_p(d_recv), ctypes.c_void_p(d_out),
+                                                       int(sign), ctypes.c_void_p(stream)))
 
     def flag_buffer(self) -> int:
         p = ctypes.c_void_p()

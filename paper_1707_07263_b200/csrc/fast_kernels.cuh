@@ -411,6 +411,11 @@ struct CombArgs {
   uint32_t m_mask;        // M - 1 (M = sub_len)
   int p;                  // passes of the logical plan (digit interleave)
   long long out_w[8], sub_w[8];
+  // blocks input layout (first pass only; 0 = off): the batch item's comb rows n1 are split over source
+  // blocks of split_q rows each, split_stride elements apart -- the [src][k1][c] layout an all-to-all
+  // leaves (element n1*rps + col of item k1 at (n1 / q) * split_stride + k1 * split_bstride + (n1 % q) * rps
+  // + col); the output keeps the plan's layout
+  long long split_q, split_stride, split_bstride;
 };
 
 __device__ __forceinline__ long long final_index_dev(const CombArgs& a, long long sub) {
@@ -564,8 +569,17 @@ struct CombTmaArgs {
   long long r_off, pitch, col_off;
   int rows_per_rank, nranks;
   int copy_only;            // diagnostics: 1 = skip the butterflies, 2 = skip the inter-pass roots
+  long long split_q;        // blocks input layout (CombArgs::split_q): 5-D tensor map, rows n1 -> (n1 % q, n1 / q)
   void* peers[16];
 };
+
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
                                             uint64_t* bar) {
@@ -611,8 +625,15 @@ k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs 
     int c0, c2, c3;
     coords(tile, c0, c2, c3);
     mbar_arrive_expect_tx(&full[s], Cfg::TILE_BYTES);
+    if (MODE == 0 && a.split_q > 0) {
+      const int q = (int)a.split_q;
 #pragma unroll 1
-    for (int n0 = 0; n0 < L; n0 += Cfg::BL) tma_load_4d(slots + s * Cfg::TILE + n0 * F, &tmap, c0, n0, c2, c3, &full[s]);
+      for (int n0 = 0; n0 < L; n0 += Cfg::BL)
+        tma_load_5d(slots + s * Cfg::TILE + n0 * F, &tmap, c0, n0 % q, n0 / q, c3, 0, &full[s]);
+    } else {
+#pragma unroll 1
+      for (int n0 = 0; n0 < L; n0 += Cfg::BL) tma_load_4d(slots + s * Cfg::TILE + n0 * F, &tmap, c0, n0, c2, c3, &full[s]);
+    }
   };
   const long long G = gridDim.x;
   long long tile = blockIdx.x;

@@ -148,6 +148,22 @@ bool encode_comb_map(CUtensorMap* map, const Pass& ps, const void* in) {
   for (int i = 0; i < 3; ++i)
     if (strides[i] % 16 != 0 || strides[i] >= (1ull << 40)) return false;
   if (dims[0] < (cuuint64_t)(Cfg::F * W) && ps.kind == K_COMB1D) return false;
+  if (ps.kind == K_COMB1D && a.split_q > 0) {
+    // blocks layout: {column, n1 % q, n1 / q, batch item, 1}; a box of BL rows spans min(BL, q) x BL/min(BL, q)
+    const long long q = a.split_q;
+    if (L % q != 0) return false;
+    const long long qb = q < Cfg::BL ? q : Cfg::BL;
+    const cuuint64_t d5[5] = {(cuuint64_t)(a.rps * W), (cuuint64_t)q, (cuuint64_t)(L / q), (cuuint64_t)B, 1};
+    const cuuint64_t s5[4] = {(cuuint64_t)(a.rps * vb), (cuuint64_t)(a.split_stride * vb),
+                              (cuuint64_t)(a.split_bstride * vb), (cuuint64_t)(a.split_bstride * vb)};
+    for (int i = 0; i < 4; ++i)
+      if (s5[i] % 16 != 0 || s5[i] >= (1ull << 40)) return false;
+    const cuuint32_t b5[5] = {(cuuint32_t)(Cfg::F * W), (cuuint32_t)qb, (cuuint32_t)(Cfg::BL / qb), 1, 1};
+    const cuuint32_t e5[5] = {1, 1, 1, 1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, const_cast<void*>(in), d5, s5, b5, e5,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   const cuuint32_t box[4] = {(cuuint32_t)(Cfg::F * W), (cuuint32_t)Cfg::BL, 1, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(in), dims, strides, box, estr,
@@ -178,6 +194,7 @@ int launch_comb_tma(const Pass& ps, const CUtensorMap& map, void* out, const voi
   a.fb = c.fb;
   a.p = c.p;
   a.m_mask = c.m_mask;
+  a.split_q = c.split_q;
   if (const char* e = std::getenv("TILEFFT_DEBUG_COPYONLY")) a.copy_only = std::atoi(e);
   for (int i = 0; i < 8; ++i) {
     a.out_w[i] = c.out_w[i];
@@ -206,7 +223,7 @@ int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, const
   // 4-comb tiles spread the pass over every SM
   if constexpr (std::is_same<Real, float>::value && L >= 64) {
     constexpr int FS = 4;
-    if (ps.kind == K_COMB1D && ps.comb.ntiles < 2LL * sm_count() && ps.comb.rps % 16 == 0) {
+    if (ps.kind == K_COMB1D && ps.comb.ntiles < 2LL * sm_count() && ps.comb.rps % 16 == 0 && ps.comb.split_q == 0) {
       using CfgS = tfb::CombCfg<float, L, FS>;
       tfb::CombArgs a = ps.comb;
       a.chunks *= 16 / FS;
@@ -238,6 +255,7 @@ int launch_comb(const Pass& ps, const void* in, void* out, const void* tb, const
       return launch_comb_tma<Real, L, INV, tfb::FOf<Real>::v>(ps, map, out, tb, tb64, scale, st);
     }
   }
+  if (ps.comb.split_q > 0) return fail(TILEFFT_EINVAL, "blocks input layout needs the TMA comb pass (16-byte aligned input)");
   using Cfg = tfb::CombCfg<Real, L>;
   auto go = [&](auto k) -> int {
     if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;

@@ -171,8 +171,10 @@ struct tilefft_plan_s {
   unsigned* peer_flags[16] = {};  // every rank's arrival word (own included), set by tilefft_dist_set_flags
   bool flags_set = false;
   tilefft_plan_s* inner = nullptr;  // row FFTs of length n2 over the rank's n1/nranks rows
+  tilefft_plan_s* inner_blocks = nullptr;  // the same, reading the [src][k1][c] blocks an all-to-all leaves
   ~tilefft_plan_s() {
     if (inner) tilefft_plan_destroy(inner);
+    if (inner_blocks) tilefft_plan_destroy(inner_blocks);
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (exec_done) cudaEventDestroy(exec_done);
@@ -1246,8 +1248,28 @@ int tilefft_dist_plan_create(tilefft_plan_t* out, uint64_t n, uint32_t nranks, u
     P->dev_factors = {n1};
     int rc = finish_plan<Real>(P, tb);
     if (rc) return rc;
-    return tilefft_plan_create(&P->inner, n2, n1 / nranks, nullptr, 0, elem_bytes, TILEFFT_MODE_FAST, nullptr, 0,
-                               device);
+    rc = tilefft_plan_create(&P->inner, n2, n1 / nranks, nullptr, 0, elem_bytes, TILEFFT_MODE_FAST, nullptr, 0,
+                             device);
+    if (rc) return rc;
+    // pass 2 straight from the all-to-all's receive buffer [src][k1][c] (NCCL exchange): the row plan
+    // with its first (comb) pass reading through a 5-D tensor map; only when that pass is a comb pass
+    if (P->inner->passes.size() > 1 && P->inner->passes[0].kind == K_COMB1D) {
+      rc = tilefft_plan_create(&P->inner_blocks, n2, n1 / nranks, nullptr, 0, elem_bytes, TILEFFT_MODE_FAST, nullptr,
+                               0, device);
+      if (rc) return rc;
+      tfb::CombArgs& c = P->inner_blocks->passes[0].comb;
+      const uint64_t C = n2 / nranks;
+      c.split_q = (long long)(C / (uint64_t)c.rps);
+      c.split_stride = (long long)((n1 / nranks) * C);
+      c.split_bstride = (long long)C;
+      if (c.split_q < 1 || C % (uint64_t)c.rps) {
+        tilefft_plan_destroy(P->inner_blocks);
+        P->inner_blocks = nullptr;
+      } else {
+        P->inner_blocks->passes_alt.clear();  // the blocks layout has no non-TMA variant
+      }
+    }
+    return 0;
   };
   int rc = elem_bytes == 8 ? build(TableBuilder<float>{}) : build(TableBuilder<double>{});
   P->tb64 = nullptr;
@@ -1313,6 +1335,16 @@ int tilefft_dist_exec_pass2(tilefft_plan_t P, const void* d_rows, void* d_out, i
   g_err.clear();
   if (!P || !P->is_dist) return fail(TILEFFT_EINVAL, "tilefft_dist_exec_pass2: not a distributed plan");
   return tilefft_exec_c2c(P->inner, d_rows, d_out, sign, stream);
+}
+
+int tilefft_dist_exec_pass2_blocks(tilefft_plan_t P, const void* d_recv, void* d_out, int sign, void* stream) {
+  g_err.clear();
+  if (!P || !P->is_dist) return fail(TILEFFT_EINVAL, "tilefft_dist_exec_pass2_blocks: not a distributed plan");
+  if (!P->inner_blocks)
+    return fail(TILEFFT_EINVAL, "tilefft_dist_exec_pass2_blocks: the row plan (n/N1 = %llu points) is a single pass; "
+                "assemble the rows and use tilefft_dist_exec_pass2", (unsigned long long)P->n2);
+  if ((uintptr_t)d_recv % 16) return fail(TILEFFT_EINVAL, "tilefft_dist_exec_pass2_blocks: input must be 16-byte aligned");
+  return tilefft_exec_c2c(P->inner_blocks, d_recv, d_out, sign, stream);
 }
 
 int tilefft_dist_flag_buffer(tilefft_plan_t P, void** d_flags) {

@@ -17,8 +17,9 @@
       transpose rides NVLink inside the kernel, overlapped tile by tile with the
       butterflies (the fused compute + all-to-all);
     - ``"nccl"``: pass 1 writes per-destination staging blocks, then one
-      ``all_to_all_single`` (NCCL grouped send/recv) and a local re-assembly
-      (one strided copy; the comparison path, not the product).
+      ``all_to_all_single`` (NCCL grouped send/recv); pass 2 reads the receive
+      buffer [src][k1][c] through a 5-D tensor map (one strided re-assembly
+      copy only when the row plan is a single pass). The comparison path.
   With GPU ops the p2p step is ``tilefft_dist_exec``: pass 1, a one-thread
   peer-flag barrier kernel and pass 2 queued on one stream (no host
   synchronisation, CUDA-graph capturable).
@@ -99,6 +100,10 @@ class GpuOps:
 
     def pass2(self, rows, out, sign):
         self.plan.pass2(rows.data_ptr(), out.data_ptr(), sign, self.stream())
+
+    def pass2_blocks(self, recv, out, sign):
+        """pass 2 reading the all-to-all receive buffer [src][R][C] in place (raises if the row plan is one pass)."""
+        self.plan.pass2_blocks(recv.data_ptr(), out.data_ptr(), sign, self.stream())
 
     def sync(self):
         self.torch.cuda.synchronize(self.device)
@@ -200,6 +205,13 @@ class DistributedFFT:
             self.dist.barrier()   # ... and so are everyone else's into our slab
         elif self.exchange == "nccl":
             self.dist.all_to_all_single(self.recv, self.stage)
+            if getattr(self, "_blocks", hasattr(o, "pass2_blocks")):
+                try:  # pass 2 reads the [src][k1][c] receive buffer through a 5-D tensor map: no re-assembly
+                    o.pass2_blocks(self.recv, out, sign)
+                    self._blocks = True
+                    return out
+                except ValueError:
+                    self._blocks = False  # single-pass row plan: assemble the rows instead
             # [src][k1][c] -> [k1][src*C + c]: one strided copy
             self.rows.view(o.r, self.world, o.c).copy_(self.recv.permute(1, 0, 2))
         o.pass2(self.rows, out, sign)

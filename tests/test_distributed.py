@@ -469,3 +469,40 @@ def test_distributed_two_processes_cuda_ipc(oracle, per_rank_gpu):
         got = assemble_output([gathered[r][call] for r in range(world)], n)
         want = oracle.fft_tiled(oracle.random_bench_signal(n, seed).astype(np.complex64))
         assert rel_l2(got, want) < 5e-7, call
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,world", [(1 << 24, 2), (1 << 24, 4), (1 << 26, 8)])
+def test_distributed_pass2_reads_alltoall_blocks(oracle, n, world):
+    """NCCL-exchange layout: pass 1 stages per-destination blocks, the all-to-all (simulated: rank d receives
+    block d of every source) leaves [src][k1][c], and pass 2 reads that buffer through its 5-D tensor map
+    (tilefft_dist_exec_pass2_blocks) -- no re-assembly copy; vs the oracle."""
+    import torch
+    from paper_1707_07263_b200 import _capi
+    from paper_1707_07263_b200.distributed import assemble_output, column_slab
+    from oracle_lib import rel_l2
+    x = oracle.random_bench_signal(n, 7).astype(np.complex64)
+    plans = [_capi.DistPlan.create_dist(n, world, g, 8, 0) for g in range(world)]
+    lay = plans[0].layout()
+    n2, c, r = lay["n2"], lay["cols_per_rank"], lay["rows_per_rank"]
+    stage = [torch.zeros((world, r, c), dtype=torch.complex64, device="cuda") for _ in range(world)]
+    for g, p in enumerate(plans):
+        p.set_peers([stage[g][d].data_ptr() for d in range(world)], c, 0)
+        p.pass1(torch.from_numpy(column_slab(x, world, g)).cuda().data_ptr())
+    torch.cuda.synchronize()
+    recv = [torch.stack([stage[s][d] for s in range(world)]).contiguous() for d in range(world)]
+    outs = [torch.empty((r, n2), dtype=torch.complex64, device="cuda") for _ in range(world)]
+    for d, p in enumerate(plans):
+        p.pass2_blocks(recv[d].data_ptr(), outs[d].data_ptr())
+    torch.cuda.synchronize()
+    got = assemble_output([o.cpu().numpy() for o in outs], n)
+    err = rel_l2(got, oracle.fft_tiled(x))
+    assert err < 5e-7, err
+
+
+@pytest.mark.gpu
+def test_distributed_pass2_blocks_needs_multipass_rows(oracle):
+    from paper_1707_07263_b200 import _capi
+    p = _capi.DistPlan.create_dist(1 << 20, 2, 0, 8, 0)  # 1024-point rows: a single pass
+    with pytest.raises(ValueError, match="single pass"):
+        p.pass2_blocks(0x1000, 0x1000)
