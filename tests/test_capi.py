@@ -70,3 +70,42 @@ def test_argument_errors_are_einval(lib):
     assert lib.tilefft_plan_create(ctypes.byref(h), 32, 1, None, 0, 8, 1, None, 0, 0) == _capi.EINVAL
     assert "empty plan" in lib.tilefft_last_error().decode()
     assert lib.tilefft_exec_c2c(None, None, None, -1, None) == _capi.EINVAL
+
+
+def test_round2_entry_points_reject_bad_arguments(lib):
+    """Null-plan / null-buffer / bad-argument paths of the round-2 entry points return EINVAL with a message
+    (no device work, so this runs without a GPU too)."""
+    from paper_1707_07263_b200 import _capi
+    ms = (ctypes.c_float * 4)()
+    assert lib.tilefft_exec_c2c_timed(None, None, None, -1, None, 1, ms, 4) == _capi.EINVAL
+    assert "null plan" in lib.tilefft_last_error().decode()
+    assert lib.tilefft_dist_exec(None, None, None, -1, None) == _capi.EINVAL
+    assert "not a distributed plan" in lib.tilefft_last_error().decode()
+    assert lib.tilefft_dist_exec_pass2_blocks(None, None, None, -1, None) == _capi.EINVAL
+    assert lib.tilefft_dist_set_flags(None, None, 0) == _capi.EINVAL
+    p = ctypes.c_void_p()
+    assert lib.tilefft_dist_flag_buffer(None, ctypes.byref(p)) == _capi.EINVAL
+    assert lib.tilefft_ipc_get_handle(None, None, None) == _capi.EINVAL
+    assert lib.tilefft_ipc_open_handle(None, 0, None) == _capi.EINVAL
+
+
+@pytest.mark.gpu
+def test_timed_exec_and_dist_guards(lib):
+    """exec_c2c_timed reports one positive time per pass; a distributed plan refuses tilefft_dist_exec until its
+    barrier words are set and rejects a flag list whose own entry is not its own buffer."""
+    import torch
+    from paper_1707_07263_b200 import _capi
+    dp = _capi.DevicePlan.create(1 << 20, 1, None, 8, _capi.MODE_FAST, None, 0)
+    x = torch.randn(1 << 20, dtype=torch.complex64, device="cuda")
+    y = torch.empty_like(x)
+    ms = dp.exec_timed(x.data_ptr(), y.data_ptr(), reps=3)
+    assert len(ms) == dp.info()["passes"] == 2 and all(v > 0 for v in ms)
+    with pytest.raises(ValueError, match="reps"):
+        _capi.check(lib.tilefft_exec_c2c_timed(dp._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                               -1, None, 0, (ctypes.c_float * 2)(), 2))
+    d0 = _capi.DistPlan.create_dist(1 << 20, 2, 0, 8, 0)
+    d1 = _capi.DistPlan.create_dist(1 << 20, 2, 1, 8, 0)
+    with pytest.raises(ValueError, match="barrier flags not set"):
+        d0.exec_step(x.data_ptr(), y.data_ptr())
+    with pytest.raises(ValueError, match="own flag buffer"):
+        d0.set_flags([d1.flag_buffer(), d0.flag_buffer()])
