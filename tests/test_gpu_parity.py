@@ -246,3 +246,28 @@ def test_one_plan_two_streams_concurrently(tf, oracle, case):
         torch.cuda.synchronize()
         for y, want in zip(ys, serial):
             assert bits_equal(y.cpu().numpy(), want), rep
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,b", [(1 << 18, 8), (1 << 22, 2), (1 << 14, 64)])
+def test_fast_batched_multipass_inplace_comb(tf, oracle, n, b):
+    """Batched multi-pass plans through the in-place-exchange TMA comb kernel and the persistent final pass:
+    every transform against the oracle, device path == host path, and an 8-byte-aligned input (no TMA: the
+    register comb kernel) within the same tolerance."""
+    import torch
+    x = oracle.random_bench_signal(n * b, 12).astype(np.complex64).reshape(b, n)
+    want = oracle.fft_tiled(x)
+    got = tf.fft_tiled(x, tf.make_plan(n))
+    per = np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)
+    assert per.max() < 5e-7, per.max()
+    xd = torch.from_numpy(x).cuda()
+    assert bits_equal(tf.fft_tiled_device(xd, tf.make_plan(n)).cpu().numpy(), got)
+    buf = torch.zeros(n * b + 1, dtype=torch.complex64, device="cuda")
+    buf[1:] = xd.reshape(-1)
+    un = buf[1:].view(b, n)
+    assert un.data_ptr() % 16 == 8
+    tf.tilefft._plan_cache.clear()
+    got_u = tf.fft_tiled_device(un, tf.make_plan(n)).cpu().numpy()
+    tf.tilefft._plan_cache.clear()
+    per_u = np.linalg.norm(got_u - want, axis=1) / np.linalg.norm(want, axis=1)
+    assert per_u.max() < 5e-7, per_u.max()
