@@ -147,3 +147,48 @@ def test_1d_2e30_distributed_virtual_ranks_vs_reference(ref_2e30, world):
     got = assemble_output(outs, n)
     del outs
     _check_2e30(got, ref_2e30)
+
+
+def test_1d_2e26_bench_plan_inverse_and_host_path(reference):
+    """The 2^26 plan's inverse (ifft_tiled: conjugate trick + 1/n, tiled_fft.hpp:410-423) vs the reference's
+    own ifft on the same input, and the host-buffer entry point (the e2e leg) bitwise equal to the device path."""
+    import torch
+    import bench
+    from paper_1707_07263_b200 import _capi
+    n = 1 << 26
+    plan = bench.make_device_plan("1d_2e26")
+    x = reference.random_bench_signal(n, 4).astype(np.complex64)
+    xd = torch.from_numpy(x.view(np.float32)).cuda()
+    yd = torch.empty_like(xd)
+    plan.exec_device(xd.data_ptr(), yd.data_ptr(), _capi.INVERSE, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    got = yd.cpu().numpy().view(np.complex64)
+    want = reference.fft_tiled(x, 1024, threads=THREADS, inverse=True)
+    err = rel_l2(got, want)
+    assert err <= tol(n) and err < 5e-7, err
+    hout = np.empty_like(x)
+    plan.exec_host(x.ctypes.data, hout.ctypes.data, _capi.INVERSE)
+    assert np.array_equal(hout.view(np.uint32), got.view(np.uint32))
+    del xd, yd
+    torch.cuda.empty_cache()
+
+
+def test_2d_8192_bench_plan_inverse_roundtrip(oracle):
+    """ifft2(fft2(x)) == x on the timed 8192^2 plan (both directions through the two-level column pass)."""
+    import torch
+    import bench
+    from paper_1707_07263_b200 import _capi
+    n = 8192
+    plan = bench.make_device_plan("2d_8192")
+    x = oracle.splitmix_signal(n * n, 5)
+    xd = torch.from_numpy(x.view(np.float32)).cuda()
+    yd = torch.empty_like(xd)
+    st = torch.cuda.current_stream().cuda_stream
+    plan.exec_device(xd.data_ptr(), yd.data_ptr(), _capi.FORWARD, st)
+    plan.exec_device(yd.data_ptr(), yd.data_ptr(), _capi.INVERSE, st)
+    torch.cuda.synchronize()
+    back = yd.cpu().numpy().view(np.complex64)
+    err = rel_l2(back, x)
+    assert err <= tol(n * n) and err < 1e-6, err
+    del xd, yd
+    torch.cuda.empty_cache()
