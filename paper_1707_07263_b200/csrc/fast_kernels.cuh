@@ -416,6 +416,14 @@ struct CombArgs {
   // leaves (element n1*rps + col of item k1 at (n1 / q) * split_stride + k1 * split_bstride + (n1 % q) * rps
   // + col); the output keeps the plan's layout
   long long split_q, split_stride, split_bstride;
+  // transposed hand-over between the first two passes of a 3-pass plan [L0][L1][L2] whose first comb
+  // stride is megabytes (pass-0 rows 8 MB apart at 2^30): pass 0 stores spectrum k0 of column
+  // c = c1*L2 + c2 at T[c1][k0][c2] (t_l2 = L2, t_l0l2 = L0*L2: its store rows L2 elements apart instead of
+  // L1*L2), pass 1 (in_t = 1) reads its comb over c1 for fixed k0 from that layout and stores the natural
+  // [k0][k1][c2] layout (rows L2 apart) out of place. A strided TMA copy that WRITES rows 8 MB apart runs at
+  // 4.5 TB/s, one that only READS them at 6.1 TB/s (profiles/r02_comb_layout.txt).
+  long long t_l2, t_l0l2;
+  int in_t;
 };
 
 __device__ __forceinline__ long long final_index_dev(const CombArgs& a, long long sub) {
@@ -468,6 +476,15 @@ __device__ __forceinline__ void comb_tile(const C2<Real>* in, C2<Real>* out, con
     in_base = batch * a.bstride + u * a.sub_len + chunk * F;
     out_base = in_base;
     s_in = s_out = a.rps;
+    if (a.in_t) {  // T[c1][k0][c2] input (see CombArgs::t_l2)
+      in_base = batch * a.bstride + u * a.rps + chunk * F;
+      s_in = a.groups_per_batch * a.rps;
+    }
+    if (a.t_l2) {
+      const long long c0 = chunk * F;
+      out_base = batch * a.bstride + (c0 / a.t_l2) * a.t_l0l2 + c0 % a.t_l2;
+      s_out = a.t_l2;
+    }
     r = (uint32_t)(chunk * F + f);
   } else {
     const long long sub = u / a.rps, rr = u % a.rps;
@@ -569,6 +586,8 @@ struct CombTmaArgs {
   long long r_off, pitch, col_off;
   int rows_per_rank, nranks;
   int copy_only;            // diagnostics: 1 = skip the butterflies, 2 = skip the inter-pass roots
+  long long t_l2, t_l0l2;   // transposed pass-0 store / pass-1 load (CombArgs::t_l2)
+  int in_t;
   long long split_q;        // blocks input layout (CombArgs::split_q): 5-D tensor map, rows n1 -> (n1 % q, n1 / q)
   void* peers[16];
 };
@@ -616,6 +635,10 @@ k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs 
     if constexpr (MODE == 0 || MODE == 2) {
       c2 = 0;
       c3 = (int)(batch * a.groups_per_batch + u);
+      if (MODE == 0 && a.in_t) {  // map {c2, c1, k0, batch} over T[c1][k0][c2]
+        c2 = (int)u;
+        c3 = (int)batch;
+      }
     } else {
       c2 = (int)(u % a.rps);
       c3 = (int)(batch * (a.groups_per_batch / a.rps) + u / a.rps);
@@ -666,6 +689,11 @@ k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs 
     if constexpr (MODE == 0) {
       out_base = batch * a.bstride + u * a.sub_len + chunk * F;
       s_out = a.rps;
+      if (a.t_l2) {
+        const long long c0 = chunk * F;
+        out_base = batch * a.bstride + (c0 / a.t_l2) * a.t_l0l2 + c0 % a.t_l2;
+        s_out = a.t_l2;
+      }
       r = (uint32_t)(chunk * F + f);
     } else if constexpr (MODE == 2) {
       out_base = a.col_off + chunk * F;

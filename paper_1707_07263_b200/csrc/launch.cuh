@@ -128,7 +128,16 @@ bool encode_comb_map(CUtensorMap* map, const Pass& ps, const void* in) {
   const long long B = a.ntiles / (a.chunks * a.groups_per_batch);
   cuuint64_t dims[4], strides[3];
   const long long vb = (long long)sizeof(tfb::C2<Real>);
-  if (ps.kind == K_COMB1D) {
+  if (ps.kind == K_COMB1D && a.in_t) {
+    // T[c1][k0][c2] (CombArgs::t_l2): {column c2, comb step c1, group k0, batch item}
+    dims[0] = (cuuint64_t)(a.rps * W);
+    dims[1] = L;
+    dims[2] = (cuuint64_t)a.groups_per_batch;
+    dims[3] = (cuuint64_t)B;
+    strides[0] = (cuuint64_t)(a.groups_per_batch * a.rps * vb);
+    strides[1] = (cuuint64_t)(a.rps * vb);
+    strides[2] = (cuuint64_t)(a.bstride * vb);
+  } else if (ps.kind == K_COMB1D) {
     dims[0] = (cuuint64_t)(a.rps * W);
     dims[1] = L;
     dims[2] = 1;
@@ -195,6 +204,9 @@ int launch_comb_tma(const Pass& ps, const CUtensorMap& map, void* out, const voi
   a.p = c.p;
   a.m_mask = c.m_mask;
   a.split_q = c.split_q;
+  a.t_l2 = c.t_l2;
+  a.t_l0l2 = c.t_l0l2;
+  a.in_t = c.in_t;
   if (const char* e = std::getenv("TILEFFT_DEBUG_COPYONLY")) a.copy_only = std::atoi(e);
   for (int i = 0; i < 8; ++i) {
     a.out_w[i] = c.out_w[i];

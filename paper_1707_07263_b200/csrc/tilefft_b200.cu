@@ -131,6 +131,7 @@ struct tilefft_plan_s {
   DevBuf tables64;        // fp64 inter-pass root tables
   TableBuilder<double>* tb64 = nullptr;  // plan-build scratch
   DevBuf work;            // workspace (batch * n elements)
+  DevBuf work2;           // second workspace: the transposed pass-0 -> pass-1 hand-over (CombArgs::t_l2)
   std::vector<Pass> passes_alt;  // same transform without two-level passes (used when the input is not 16-B aligned)
   DevBuf scratch, ctrl;   // two-level passes: L2-resident exchange slots and their counters
   // Replayed launch sequences: one CUDA graph per (in, out, sign), captured on
@@ -473,6 +474,24 @@ int build_fast_1d(tilefft_plan_s* P, TableBuilder<Real>& tb) {
     }
     P->passes.push_back(ps);
   }
+  // 3-pass plans: pass 0 hands over to pass 1 through the transposed T[c1][k0][c2] layout in a second
+  // workspace, so no pass writes its rows L1*L2 elements apart (CombArgs::t_l2). Measured against the
+  // in-place hand-over: 2^30 10.26 vs 10.57 ms (pass 0 3.52 vs 3.91 ms), 2^29 -4 %, 2^28 -4 %, 2^27 -3 %,
+  // 2^26 -1 % (tools/gpu/r02_tstore.sh). TILEFFT_TSTORE=0 keeps the in-place hand-over (A/B only).
+  {
+    const bool want = env_int("TILEFFT_TSTORE", 1) != 0;
+    if (want && p == 3 && g.rps[1] == f[2] && (uint64_t)P->passes[1].comb.groups_per_batch == f[0] &&
+        f[2] % kF == 0) {
+      Pass& p0 = P->passes[0];
+      Pass& p1 = P->passes[1];
+      p0.comb.t_l2 = (long long)f[2];
+      p0.comb.t_l0l2 = (long long)(f[0] * f[2]);
+      p0.dst = 3;
+      p1.comb.in_t = 1;
+      p1.src = 3;
+      p1.dst = 2;
+    }
+  }
   P->dev_factors = f;
   if (build_two_1d<Real>(P, tb)) return 0;
   return 0;
@@ -658,6 +677,13 @@ int finish_plan(tilefft_plan_s* P, TableBuilder<Real>& tb) {
     int rc = P->work.alloc(elems * sizeof(tfb::C2<Real>));
     if (rc) return rc;
   }
+  bool need_work2 = false;
+  for (const Pass& ps : P->passes) need_work2 |= (ps.src == 3 || ps.dst == 3);
+  for (const Pass& ps : P->passes_alt) need_work2 |= (ps.src == 3 || ps.dst == 3);
+  if (need_work2) {
+    int rc = P->work2.alloc(elems * sizeof(tfb::C2<Real>));
+    if (rc) return rc;
+  }
   if (P->tb64 && !P->tb64->h.empty()) {
     int rc = P->tables64.alloc(P->tb64->h.size() * sizeof(double));
     if (rc) return rc;
@@ -677,7 +703,9 @@ int exec_impl(tilefft_plan_s* P, const void* in, void* out, int sign, cudaStream
   const bool inv = sign == TILEFFT_INVERSE;
   const uint64_t total = P->is2d ? P->ny * P->nx : P->n;
   const Real scale = inv ? (Real)1 / (Real)total : (Real)1;
-  auto buf = [&](int id) -> void* { return id == 0 ? const_cast<void*>(in) : id == 1 ? out : P->work.p; };
+  auto buf = [&](int id) -> void* {
+    return id == 0 ? const_cast<void*>(in) : id == 1 ? out : id == 3 ? P->work2.p : P->work.p;
+  };
   // two-level passes stream their input with TMA (16-byte aligned); an
   // unaligned user buffer takes the equivalent plan without them
   const bool use_alt = !P->passes_alt.empty() && ((uintptr_t)in % 16 != 0);
@@ -1464,7 +1492,7 @@ int tilefft_plan_info(tilefft_plan_t P, tilefft_plan_info_t* info) {
     info->launches_per_exec = info->passes + 1;
   }
   for (size_t i = 0; i < P->dev_factors.size() && i < 16; ++i) info->factors[i] = P->dev_factors[i];
-  info->workspace_bytes = P->work.bytes;
+  info->workspace_bytes = P->work.bytes + P->work2.bytes;
   info->table_bytes = P->tables.bytes;
   return 0;
 }

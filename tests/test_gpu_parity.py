@@ -271,3 +271,45 @@ def test_fast_batched_multipass_inplace_comb(tf, oracle, n, b):
     tf.tilefft._plan_cache.clear()
     per_u = np.linalg.norm(got_u - want, axis=1) / np.linalg.norm(want, axis=1)
     assert per_u.max() < 5e-7, per_u.max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,b,dtype", [(1 << 21, 4, np.complex64), (1 << 22, 2, np.complex64),
+                                       (1 << 24, 1, np.complex64), (1 << 21, 2, np.complex128)])
+def test_fast_transposed_handover(tf, oracle, monkeypatch, n, b, dtype):
+    """3-pass plans hand over from pass 0 to pass 1 through the transposed T[c1][k0][c2] layout
+    (CombArgs::t_l2, the default): every transform against the oracle (forward, inverse), device path ==
+    host path, and a misaligned input (register comb kernel for pass 0) within the same tolerance; the plan
+    carries the second workspace. Then the same transforms with the in-place hand-over (TILEFFT_TSTORE=0)."""
+    import torch
+    for k in [k for k in __import__("os").environ if k.startswith("TILEFFT_")]:
+        monkeypatch.delenv(k)
+    tf.tilefft._plan_cache.clear()
+    x = oracle.random_bench_signal(n * b, 21).astype(dtype).reshape(b, n)
+    want = oracle.fft_tiled(x)
+    plan = tf.make_plan(n)
+    got = tf.fft_tiled(x, plan)
+    lim = 5e-7 if dtype == np.complex64 else 1e-13
+    per = np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)
+    assert per.max() < lim, per.max()
+    back = tf.ifft_tiled(got, plan)
+    assert rel_l2(back, x) < (1e-6 if dtype == np.complex64 else 1e-14)
+    xd = torch.from_numpy(x).cuda()
+    assert bits_equal(tf.fft_tiled_device(xd, plan).cpu().numpy(), got)
+    info = tf.tilefft._plan_cache and next(iter(tf.tilefft._plan_cache.values())).info()
+    if info:
+        assert len(info["factors"]) == 3, info
+        assert info["workspace_bytes"] >= 2 * n * b * x.itemsize, info
+    buf = torch.zeros(n * b + 1, dtype=xd.dtype, device="cuda")
+    buf[1:] = xd.reshape(-1)
+    un = buf[1:].view(b, n)
+    tf.tilefft._plan_cache.clear()
+    got_u = tf.fft_tiled_device(un, tf.make_plan(n)).cpu().numpy()
+    tf.tilefft._plan_cache.clear()
+    per_u = np.linalg.norm(got_u - want, axis=1) / np.linalg.norm(want, axis=1)
+    assert per_u.max() < lim, per_u.max()
+    monkeypatch.setenv("TILEFFT_TSTORE", "0")
+    got0 = tf.fft_tiled(x, tf.make_plan(n))
+    tf.tilefft._plan_cache.clear()
+    per0 = np.linalg.norm(got0 - want, axis=1) / np.linalg.norm(want, axis=1)
+    assert per0.max() < lim, per0.max()
