@@ -49,7 +49,6 @@ struct Pass {
   long long two_cols, two_es_in;  // columns along the axis and their element stride (input)
   size_t twl_off;                 // W_L^e table (L entries)
   int two_ctas;                   // persistent grid
-  int two_kernel;                 // 0 = k_two_ws, 1 = k_two_tma
 };
 
 // Distributed four-step, pass 1 on one rank (see tilefft_dist_* in the C ABI).

@@ -320,9 +320,8 @@ int launch_final(const Pass& ps, const void* in, void* out, const void* tb, cons
   return 0;
 }
 
-// Two-level pass (fp32): tensor map over the strided axis {column, n1, n2, batch}
-// (128-byte swizzle for the transposed-output variant), control block reset,
-// persistent launch.
+// Two-level pass (fp32): 128-byte-swizzled tensor maps over the strided axis {column, n1, n2, batch} and
+// over the L2 scratch ring, control block reset, persistent launch of k_two_tma (one CTA per SM).
 template <int LA, int LB, bool INV, int OUTT, bool TWID>
 int launch_two_k(const Pass& ps, const void* in, void* out, const void* tb, const void* tb64, float scale,
                  cudaStream_t st) {
@@ -332,60 +331,45 @@ int launch_two_k(const Pass& ps, const void* in, void* out, const void* tb, cons
   if ((uintptr_t)in % 16) return fail(TILEFFT_EINVAL, "two-level pass: input must be 16-byte aligned");
   const tfb::TwoArgs& a = ps.two;
   const long long B = a.groups / a.chunks;
-  CUtensorMap map;
   const cuuint64_t dims[4] = {(cuuint64_t)ps.two_cols, (cuuint64_t)LB, (cuuint64_t)LA, (cuuint64_t)B};
   const cuuint64_t strides[3] = {(cuuint64_t)(ps.two_es_in * 8), (cuuint64_t)(ps.two_es_in * 8 * LB),
                                  (cuuint64_t)(a.bs_in * 8)};
   const cuuint32_t box[4] = {16, 1, (cuuint32_t)Cfg::BL, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
-  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(in), dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, OUTT ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled failed for the two-level pass");
   const float2* t = (const float2*)tb;
   const double2* t64 = (const double2*)tb64;
-  if (ps.two_kernel != 0) {
-    // barrier-free TMA kernel (default): input tiles 128-byte swizzled, scratch read back by TMA
-    CUtensorMap tin, tscr;
-    if (enc(&tin, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(in), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled failed for the two-level pass");
-    const cuuint64_t sdims[4] = {(cuuint64_t)LA, 16, (cuuint64_t)LB, (cuuint64_t)a.nslot};
-    const cuuint64_t sstr[3] = {(cuuint64_t)LA * 8, (cuuint64_t)LA * 8 * 16, (cuuint64_t)LA * 8 * 16 * LB};
-    const cuuint32_t sbox[4] = {16, 16, (cuuint32_t)LB, 1};
-    if (enc(&tscr, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, a.scratch, sdims, sstr, sbox, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled failed for the two-level scratch");
-    auto launch = [&](auto kfn, int threads, int smem) -> int {
-      if (int rc = ensure_smem((const void*)kfn, smem)) return rc;
-      CUDA_TRY(cudaMemsetAsync(a.ctrl, 0, sizeof(unsigned) * (2 + 2 * a.nslot), st));
-      kfn<<<sm_count(), threads, smem, st>>>(tin, tscr, (float2*)out, a, t + ps.tw_off, t + ps.twl_off,
-                                             t64 + ps.wc_off, t64 + ps.wf_off, scale);
-      CUDA_TRY(cudaGetLastError());
-      return 0;
-    };
-    using TC = tfb::TwoTmaCfg<LA, LB>;
-    // plain column passes: the B items (a 16-point DFT, no inter-pass root) take the W_L roots off the
-    // A items' critical path (8192^2: 523 vs 532 us; tools/gpu/r02_twlb.sh)
-    // 19 compute warps at <= 96 registers (16 at 128 before): 8192^2 columns 503 vs 519 us; 23 warps
-    // (80 registers, spills) 535 us (tools/gpu/r02_cw.sh)
-    if constexpr (!TWID && OUTT == 0) {
-      using TCB = tfb::TwoTmaCfg<LA, LB, 19>;
-      return launch(tfb::k_two_tma<LA, LB, INV, OUTT, TWID, true, TCB::CW>, TCB::THREADS, TCB::SMEM);
-    }
-    return launch(tfb::k_two_tma<LA, LB, INV, OUTT, TWID>, TC::THREADS, TC::SMEM);
+  CUtensorMap tin, tscr;
+  if (enc(&tin, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(in), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled failed for the two-level pass");
+  const cuuint64_t sdims[4] = {(cuuint64_t)LA, 16, (cuuint64_t)LB, (cuuint64_t)a.nslot};
+  const cuuint64_t sstr[3] = {(cuuint64_t)LA * 8, (cuuint64_t)LA * 8 * 16, (cuuint64_t)LA * 8 * 16 * LB};
+  const cuuint32_t sbox[4] = {16, 16, (cuuint32_t)LB, 1};
+  if (enc(&tscr, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, a.scratch, sdims, sstr, sbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return fail(TILEFFT_ECUDA, "cuTensorMapEncodeTiled failed for the two-level scratch");
+  auto launch = [&](auto kfn, int threads, int smem) -> int {
+    if (int rc = ensure_smem((const void*)kfn, smem)) return rc;
+    CUDA_TRY(cudaMemsetAsync(a.ctrl, 0, sizeof(unsigned) * (2 + 2 * a.nslot), st));
+    kfn<<<sm_count(), threads, smem, st>>>(tin, tscr, (float2*)out, a, t + ps.tw_off, t + ps.twl_off,
+                                           t64 + ps.wc_off, t64 + ps.wf_off, scale);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  };
+  using TC = tfb::TwoTmaCfg<LA, LB>;
+  // plain column passes: the B items (a 16-point DFT, no inter-pass root) take the W_L roots off the
+  // A items' critical path (8192^2: 523 vs 532 us; tools/gpu/r02_twlb.sh)
+  // 19 compute warps at <= 96 registers (16 at 128 before): 8192^2 columns 503 vs 519 us; 23 warps
+  // (80 registers, spills) 535 us (tools/gpu/r02_cw.sh)
+  // (the round-1 team-split kernel k_two_ws -- A and B teams behind named barriers -- measured slower
+  // and was removed in round 2: 8192^2 column pass 341 us in round 1, k_two_tma 297 us)
+  if constexpr (!TWID && OUTT == 0) {
+    using TCB = tfb::TwoTmaCfg<LA, LB, 19>;
+    return launch(tfb::k_two_tma<LA, LB, INV, OUTT, TWID, true, TCB::CW>, TCB::THREADS, TCB::SMEM);
   }
-  // warp-specialised two-level kernel: one 512-thread CTA per SM (A team + B team)
-  using WCfg = tfb::TwoWsCfg<LA, LB, INV, OUTT>;
-  auto kw = tfb::k_two_ws<LA, LB, INV, OUTT, TWID>;
-  if (int rc = ensure_smem((const void*)kw, WCfg::SMEM)) return rc;
-  CUDA_TRY(cudaMemsetAsync(a.ctrl, 0, sizeof(unsigned) * (2 + 2 * a.nslot), st));
-  kw<<<sm_count(), 512, WCfg::SMEM, st>>>(map, (float2*)out, a, t + ps.tw_off, t + ps.twl_off, t64 + ps.wc_off,
-                                           t64 + ps.wf_off, scale);
-  CUDA_TRY(cudaGetLastError());
-  return 0;
+  return launch(tfb::k_two_tma<LA, LB, INV, OUTT, TWID>, TC::THREADS, TC::SMEM);
 }
 
 template <int LA, int LB, bool INV>

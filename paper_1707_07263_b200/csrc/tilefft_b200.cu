@@ -349,7 +349,6 @@ Pass make_two_pass(tilefft_plan_s* P, TableBuilder<Real>& tb, uint64_t L, long l
   if (a.D > a.groups) a.D = (int)a.groups;
   a.nslot = std::max(a.D + 1, env_int("TILEFFT_TWO_NSLOT", a.D + 16));
   a.discard = env_int("TILEFFT_TWO_DISCARD", 1);
-  ps.two_kernel = env_int("TILEFFT_TWO_KERNEL", 1);
   a.diag = env_int("TILEFFT_TWO_DIAG", 0);
   a.trace = nullptr;
   a.watchdog = two_watchdog();

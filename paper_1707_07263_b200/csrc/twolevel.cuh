@@ -167,264 +167,6 @@ __device__ __forceinline__ void discard_l2(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 
-// ---------------------------------------------------------------- K_TWO_WS
-// Warp-specialised K_TWO: one persistent CTA per SM holds an A team (warps
-// 0-7) and a B team (warps 8-15) with their own item counters and named
-// barriers, so one team's waits (TMA tile, L2 round trip of the scratch,
-// the release fence after each item) overlap the other team's arithmetic
-// instead of stalling a CTA-wide __syncthreads. The A team streams its tiles
-// through a 2-slot TMA ring (the next tile loads while the current one is
-// transformed). Items are still handed out in group order, so the oldest
-// outstanding item of either kind only depends on older ones: with every CTA
-// resident (grid <= SMs), spinning cannot deadlock.
-//
-// ctrl: [0] A counter, [1..nslot] A done, [nslot+1..2 nslot] B done,
-//       [2 nslot + 1] B counter.
-template <int ID>
-struct SyncNamed {
-  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, 256;" ::"n"(ID) : "memory"); }
-};
-
-template <int LA, int LB, bool INV, int OUTT>
-struct TwoWsCfg {
-  // half-tile exchange buffer (2 rounds): a full one (1 round, 192 KB of shared
-  // memory) measured slower twice (618 vs 585 us, then 612 vs 536 us at 8192^2)
-  using Base = TwoCfg<LA, LB, INV, OUTT, 2>;
-  static constexpr int NS = 2;  // A tile slots
-  // (exchanging in place in the consumed tile slot -- one round, slot refilled
-  // after the FFT -- measured slower at 8192^2: 615 vs 550 us with 2 or 3 slots)
-  static constexpr int SMEM = NS * Base::TILE_BYTES + Base::XB * 8 + NS * 8 + 1024;
-};
-
-template <int LA, int LB, bool INV, int OUTT, bool TWID>
-__global__ void __launch_bounds__(512, 1)
-k_two_ws(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ out, TwoArgs a, const float2* __restrict__ tw,
-         const float2* __restrict__ twl, const double2* __restrict__ wc, const double2* __restrict__ wf, float scale) {
-  using Cfg = typename TwoWsCfg<LA, LB, INV, OUTT>::Base;
-  constexpr int NS = TwoWsCfg<LA, LB, INV, OUTT>::NS;
-  // Who applies W_L^{n1 k2}: the B team when it has spare time (no inter-pass
-  // root: 8192^2 column pass 396 -> 341 us), the A team when the B team also
-  // carries the inter-pass root W_M^{c k} (TWID) and would fall behind (a
-  // lagging B team lets the scratch ring outgrow L2 and spill to DRAM).
-  constexpr bool TWL_IN_B = !TWID;
-  using V = float2;
-  using Sh = typename Cfg::Sh;
-  constexpr int F = Cfg::F, T = Cfg::T, KB = Cfg::KB;
-  extern __shared__ unsigned char smem_raw[];
-  // align by pointer arithmetic: an integer round trip would lose the shared
-  // address space and turn every tile access into a generic LD.E/ST.E
-  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  V* tiles = reinterpret_cast<V*>(base);
-  V* xb = tiles + NS * Cfg::TILE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(xb + Cfg::XB);
-  __shared__ long long s_a_g[NS];
-  __shared__ int s_a_sub[NS];
-  __shared__ long long s_b_id;
-  const int team = threadIdx.x >> 8, tid = threadIdx.x & 255;
-  const long long G = a.groups;
-  const long long NA = G * LB;  // items of each kind
-  unsigned* doneA = a.ctrl + 1;
-  unsigned* doneB = a.ctrl + 1 + a.nslot;
-  unsigned* workA = a.ctrl;
-  unsigned* workB = a.ctrl + 1 + 2 * a.nslot;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-
-  if (team == 0) {
-    // ============================================================ A team
-    SyncNamed<1> sy;
-    auto grab_into = [&](int s) {
-      const long long id = (long long)atomicAdd(workA, 1u);
-      if (id < NA) {
-        const long long g = id / LB;
-        const int n1 = (int)(id % LB);
-        const long long b = g / a.chunks, ch = g % a.chunks;
-        mbar_arrive_expect_tx(&full[s], Cfg::TILE_BYTES);
-#pragma unroll 1
-        for (int r = 0; r < LA; r += Cfg::BL)
-          tma_load_4d_l2(tiles + s * Cfg::TILE + r * F, &tmap, (int)(ch * F), n1, r, (int)b, &full[s]);
-        s_a_g[s] = g;
-        s_a_sub[s] = n1;
-      } else {
-        s_a_g[s] = -1;
-      }
-    };
-    if (tid == 0)
-      for (int s = 0; s < NS; ++s) grab_into(s);
-    sy();
-#pragma unroll 1
-    for (int k = 0;; ++k) {
-      const int s = k % NS;
-      const long long g = s_a_g[s];
-      const int n1 = s_a_sub[s];
-      if (g < 0) break;
-      const int slot = (int)(g % a.nslot);
-      const unsigned gen = (unsigned)(g / a.nslot);
-      V* scr = reinterpret_cast<V*>(a.scratch) + (size_t)slot * Cfg::GROUP;
-      mbar_wait(&full[s], (uint32_t)((k / NS) & 1));
-      const V* tile = tiles + s * Cfg::TILE;
-      V v[Sh::R];
-      int t, f;
-      if constexpr (OUTT == 0) {
-        f = tid % F;
-        t = tid / F;
-#pragma unroll
-        for (int q = 0; q < Sh::R; ++q) v[q] = tile[(t + q * T) * F + f];
-      } else {
-        f = tid / T;
-        t = tid % T;
-#pragma unroll
-        for (int q = 0; q < Sh::R; ++q) {
-          const int n2 = t + q * T;
-          v[q] = tile[n2 * F + ((((f >> 1) ^ (n2 & 7))) << 1) + (f & 1)];
-        }
-      }
-      const int my_round = f / Cfg::FX, fx = f % Cfg::FX;
-      fence_proxy_async_smem();
-      sy();  // slot s consumed (and s_a_* of slot s read by every thread)
-      if (tid == 0) grab_into(s);
-      if constexpr (OUTT == 0) {
-        auto ex = [xb, fx](int i) -> V& { return xb[i * Cfg::FX + fx]; };
-        Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
-      } else {
-        V* reg = xb + fx * Cfg::REG;
-        auto ex = [reg](int i) -> V& { return reg[pad32(i)]; };
-        Stages<V, LA, 32, INV, 0, Cfg::NR>::run(v, t, ex, tw, sy, my_round);
-      }
-      if constexpr (!TWL_IN_B) {
-#pragma unroll
-        for (int j = 0; j < Sh::R; ++j) {
-          const int k2 = out_index<LA, 32>(t, j);
-          v[j] = ctw<INV>(v[j], __ldg(twl + n1 * k2));
-        }
-      }
-      if (tid == 0 && gen > 0) wait_geq_wd(doneB + slot, gen * LB, a.watchdog, -1, 1);
-      sy();
-      if constexpr (OUTT == 0) {
-#pragma unroll
-        for (int j = 0; j < Sh::R; ++j) scr[((size_t)n1 * LA + out_index<LA, 32>(t, j)) * F + f] = v[j];
-      } else {
-#pragma unroll
-        for (int j = 0; j < Sh::R; ++j) scr[((size_t)n1 * F + f) * LA + out_index<LA, 32>(t, j)] = v[j];
-      }
-      // (a per-warp release without this barrier measured slower: 356 vs 341 us)
-      sy();
-      if (tid == 0) signal_release(doneA + slot);
-    }
-  } else {
-    // ============================================================ B team
-    SyncNamed<2> sy;
-#pragma unroll 1
-    for (;;) {
-      if (tid == 0) {
-        const long long id = (long long)atomicAdd(workB, 1u);
-        s_b_id = id;
-        if (id < NA) {
-          const long long g = id / LB;
-          wait_geq_wd(doneA + (int)(g % a.nslot), (unsigned)(g / a.nslot + 1) * LB, a.watchdog, id, 2);
-        }
-      }
-      sy();
-      const long long id = s_b_id;
-      if (id >= NA) break;
-      const long long g = id / LB;
-      const int kb = (int)(id % LB);
-      const int slot = (int)(g % a.nslot);
-      const V* scr = reinterpret_cast<const V*>(a.scratch) + (size_t)slot * Cfg::GROUP;
-      const long long b = g / a.chunks, ch = g % a.chunks;
-#pragma unroll
-      for (int m = 0; m < Cfg::PAIRS; ++m) {
-        const int p = tid + 256 * m;
-        int f, k2l;
-        if constexpr (OUTT == 0) {
-          f = p % F;
-          k2l = p / F;
-        } else {
-          k2l = p % KB;
-          f = p / KB;
-        }
-        const int k2 = kb * KB + k2l;
-        V v[LB];
-#pragma unroll
-        for (int n1 = 0; n1 < LB; ++n1) {
-          const V* q = OUTT == 0 ? scr + ((size_t)n1 * LA + k2) * F + f : scr + ((size_t)n1 * F + f) * LA + k2;
-          v[n1] = __ldcg(q);
-        }
-        // W_L^{n1 k2}, deferred from the A item when the A team is the critical path
-        if constexpr (TWL_IN_B) {
-#pragma unroll
-          for (int n1 = 1; n1 < LB; ++n1) v[n1] = ctw<INV>(v[n1], __ldg(twl + n1 * k2));
-        }
-        reg_dft<LB, INV>(v);
-        const long long c = ch * F + f;
-        if constexpr (TWID) {
-          // W_M^{c (k2 + LA k1)} = B[k1 % 4] * A[k1 / 4] with B[b] = W^{c k2} s^b,
-          // A[a] = s^{4a}, s = W^{c LA}: built in fp64 (depth ~4 instead of a
-          // 15-long dependent chain), each rounded once, product in fp32
-          constexpr int QA = LB / 4 > 0 ? LB / 4 : 1;
-          const double2 w0 = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)k2) & a.m_mask, a.fb);
-          const double2 s1 = interpass_root64(wc, wf, ((uint32_t)c * (uint32_t)LA) & a.m_mask, a.fb);
-          const double2 s2 = cmul(s1, s1), s4 = cmul(s2, s2);
-          const double2 w2 = cmul(w0, s2);
-          const V Bq[4] = {to_v(w0, (V*)nullptr), to_v(cmul(w0, s1), (V*)nullptr), to_v(w2, (V*)nullptr),
-                           to_v(cmul(w2, s1), (V*)nullptr)};
-          V Aq[QA];
-          {
-            double2 p = make_double2(1.0, 0.0);
-#pragma unroll
-            for (int q = 0; q < QA; ++q) {
-              Aq[q] = to_v(p, (V*)nullptr);
-              if (q + 1 < QA) p = cmul(p, s4);
-            }
-          }
-#pragma unroll
-          for (int k1 = 0; k1 < LB; ++k1) {
-            const V w = k1 < 4 ? Bq[k1 % 4] : cmul(Aq[k1 / 4], Bq[k1 % 4]);
-            v[k1] = ctw<INV>(v[k1], w);
-          }
-        }
-        if (scale != 1.0f) {
-#pragma unroll
-          for (int k1 = 0; k1 < LB; ++k1) v[k1] = mk(v[k1].x * scale, v[k1].y * scale);
-        }
-        if constexpr (OUTT == 0) {
-          V* o = out + b * a.bs_out + c;
-#pragma unroll
-          for (int k1 = 0; k1 < LB; ++k1) o[(long long)(k2 + LA * k1) * a.es_out] = v[k1];
-        } else {
-          V* o = out + b * a.bs_out + c * a.es_out + k2;
-#pragma unroll
-          for (int k1 = 0; k1 < LB; ++k1) o[LA * k1] = v[k1];
-        }
-      }
-      sy();  // all scratch reads of this item done
-      if (a.discard) {
-        constexpr int LINES = LB * KB * F * 8 / 128;
-        for (int i = tid; i < LINES; i += 256) {
-          const V* q;
-          if constexpr (OUTT == 0) {
-            const int n1 = i / KB, k2 = kb * KB + i % KB;
-            q = scr + ((size_t)n1 * LA + k2) * F;
-          } else {
-            constexpr int LPR = KB * 8 / 128;
-            const int row = i / LPR, part = i % LPR;
-            q = scr + (size_t)row * LA + kb * KB + part * 16;
-          }
-          discard_l2(q);
-        }
-        sy();
-      }
-      if (tid == 0) {
-        signal_release(doneB + slot);
-      }
-    }
-  }
-}
-
 // ---------------------------------------------------------------- K_TWO_TMA
 // Barrier-free two-level pass. Every item, A or B, is one 64 KB shared-memory
 // slot that arrives by TMA:
