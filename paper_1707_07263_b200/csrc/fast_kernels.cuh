@@ -744,6 +744,123 @@ k_comb_tma(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs 
   }
 }
 
+// ------------------------------------------------------------------ K_COMB_H3
+// K_COMB_TMA (1D inner pass, in-place exchange) with the tile split into two
+// halves (comb steps [0, L/2) and [L/2, L)) over a ring of THREE half-tile
+// slots: when tile k's exchange has been read back, its two half-slots take
+// the second half of tile k+1 and the first half of tile k+2, so the first
+// half of every tile is requested a whole tile earlier and the wait for the
+// next tile covers only half of it. The exchange runs in place across the
+// tile's two half-slots (index i -> half i / (L/2)).
+template <typename Real, int L, int F_ = FOf<Real>::v>
+struct CombH3Cfg {
+  using Base = CombTmaCfg<Real, L, F_, true>;
+  using V = C2<Real>;
+  static constexpr int F = F_, H = L / 2;
+  static constexpr int THREADS = Base::THREADS;
+  static constexpr int HALF = H * F;                          // elements per half-tile slot
+  static constexpr int HALF_BYTES = HALF * (int)sizeof(V);
+  static constexpr int BL = Base::BL < H ? Base::BL : H;      // TMA box rows
+  static constexpr int DATA_BYTES = 3 * HALF_BYTES;
+  static constexpr int SMEM = DATA_BYTES + 3 * 8 + 128;
+  static constexpr int WARPS = Base::WARPS;
+  static constexpr int MINB_W = 16 / WARPS > 0 ? 16 / WARPS : 1;
+  static constexpr int MINB_S = (227 * 1024) / (SMEM + 1024) > 0 ? (227 * 1024) / (SMEM + 1024) : 1;
+  static constexpr int MINB = MINB_W < MINB_S ? MINB_W : MINB_S;
+};
+
+template <typename Real, int L, bool INV, int F_ = FOf<Real>::v>
+__global__ void __launch_bounds__(CombH3Cfg<Real, L, F_>::THREADS, CombH3Cfg<Real, L, F_>::MINB)
+k_comb_h3(const __grid_constant__ CUtensorMap tmap, C2<Real>* out, CombTmaArgs a, const C2<Real>* __restrict__ tw,
+          const double2* __restrict__ wc, const double2* __restrict__ wf, Real scale) {
+  using Cfg = CombH3Cfg<Real, L, F_>;
+  using V = C2<Real>;
+  using Sh = typename CombTmaCfg<Real, L, F_, true>::Sh;
+  constexpr int F = Cfg::F, H = Cfg::H;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  V* hs = reinterpret_cast<V*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + Cfg::DATA_BYTES);
+  const int f = threadIdx.x % F, t = threadIdx.x / F;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 3; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue_half = [&](long long tile, int half, int slot) {
+    const long long chunk = tile % a.chunks, g = tile / a.chunks;
+    const long long batch = g / a.groups_per_batch, u = g % a.groups_per_batch;
+    const int c0 = (int)(chunk * F * (sizeof(V) / 8));
+    int c2 = 0, c3 = (int)(batch * a.groups_per_batch + u);
+    if (a.in_t) {
+      c2 = (int)u;
+      c3 = (int)batch;
+    }
+    mbar_arrive_expect_tx(&full[slot], Cfg::HALF_BYTES);
+#pragma unroll 1
+    for (int n0 = 0; n0 < H; n0 += Cfg::BL)
+      tma_load_4d(hs + slot * Cfg::HALF + n0 * F, &tmap, c0, half * H + n0, c2, c3, &full[slot]);
+  };
+  const long long G = gridDim.x;
+  long long tile = blockIdx.x;
+  int sa = 0, sb = 1, sc = 2;  // this tile's halves in (sa, sb); the next tile's first half in sc
+  uint32_t ph = 0;             // bit s: parity of slot s's next completion
+  if (threadIdx.x == 0 && tile < a.ntiles) {
+    issue_half(tile, 0, 0);
+    issue_half(tile, 1, 1);
+    if (tile + G < a.ntiles) issue_half(tile + G, 0, 2);
+  }
+#pragma unroll 1
+  for (; tile < a.ntiles; tile += G) {
+    V* pa = hs + sa * Cfg::HALF;
+    V* pb = hs + sb * Cfg::HALF;
+    mbar_wait(&full[sa], (ph >> sa) & 1u);
+    mbar_wait(&full[sb], (ph >> sb) & 1u);
+    ph ^= (1u << sa) | (1u << sb);
+    V v[Sh::R];
+#pragma unroll
+    for (int q = 0; q < Sh::R; ++q) {
+      const int i = t + q * Sh::T;
+      v[q] = (i < H ? pa : pb)[(i & (H - 1)) * F + f];
+    }
+    __syncthreads();  // every thread has its elements before the in-place exchange overwrites them
+    const long long chunk = tile % a.chunks, g = tile / a.chunks;
+    const long long batch = g / a.groups_per_batch, u = g % a.groups_per_batch;
+    long long out_base = batch * a.bstride + u * a.sub_len + chunk * F, s_out = a.rps;
+    if (a.t_l2) {
+      const long long c0 = chunk * F;
+      out_base = batch * a.bstride + (c0 / a.t_l2) * a.t_l0l2 + c0 % a.t_l2;
+      s_out = a.t_l2;
+    }
+    const uint32_t r = (uint32_t)(chunk * F + f);
+    const long long nx = tile + G, nn = tile + 2 * G;
+    const int sb_ = sa, sc_ = sb;
+    auto refill = [&]() {
+      fence_proxy_async_smem();
+      __syncthreads();  // both half-slots fully consumed: the next tile's second half, the one after's first
+      if (threadIdx.x == 0) {
+        if (nx < a.ntiles) issue_half(nx, 1, sb_);
+        if (nn < a.ntiles) issue_half(nn, 0, sc_);
+      }
+    };
+    auto ex = [pa, pb, f](int i) -> V& { return (i < H ? pa : pb)[(i & (H - 1)) * F + f]; };
+    SyncBlock sy;
+    Stages<V, L, RmaxOf<Real>::v, INV, 0, 1>::run(v, t, ex, tw, sy, 0, refill);
+    interpass_scale<V, L, RmaxOf<Real>::v, INV>(v, t, r, a.m_mask, a.fb, wc, wf);
+#pragma unroll
+    for (int j = 0; j < Sh::R; ++j) {
+      const int kk = out_index<L, RmaxOf<Real>::v>(t, j);
+      V x = v[j];
+      if (scale != (Real)1) x = mk(x.x * scale, x.y * scale);
+      out[out_base + f + (long long)kk * s_out] = x;
+    }
+    // rotate: next tile = (sc, sa), the tile after's first half goes to sb
+    const int na = sc, nb = sa, nc = sb;
+    sa = na;
+    sb = nb;
+    sc = nc;
+  }
+}
+
 // ------------------------------------------------------------------ K_FINAL_T
 // Final pass of a multi-pass 1D plan (tiled_fft.hpp:295-306): rows are
 // contiguous on input but the digit interleave scatters each spectrum with

@@ -212,13 +212,30 @@ int launch_comb_tma(const Pass& ps, const CUtensorMap& map, void* out, const voi
     a.out_w[i] = c.out_w[i];
     a.sub_w[i] = c.sub_w[i];
   }
+  const V* t = (const V*)tb;
+  const double2* t64 = (const double2*)tb64;
+  // L >= 512: the tile over three half-tile slots (k_comb_h3) -- the first half of every tile requested a
+  // tile earlier: 2^26 -1.1 %, 2^28 -2.5 %, 2^29 -1 %, 2^30 -0.3 % (tools/gpu/r02_h3.sh); TILEFFT_COMB_H3=0 = A/B
+  if constexpr (IP && L >= 512 && F == tfb::FOf<Real>::v) {
+    static const int h3 = env_int_or("TILEFFT_COMB_H3", 1);
+    if (h3 && c.split_q == 0 && a.copy_only == 0) {
+      using C3 = tfb::CombH3Cfg<Real, L, F>;
+      auto k3 = tfb::k_comb_h3<Real, L, INV, F>;
+      if (int rc = ensure_smem((const void*)k3, C3::SMEM)) return rc;
+      int b3 = 0;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, k3, C3::THREADS, C3::SMEM));
+      const long long g3 = std::max<long long>(1, std::min<long long>(a.ntiles, (long long)sm_count() * std::max(b3, 1)));
+      k3<<<(unsigned)g3, C3::THREADS, C3::SMEM, st>>>(map, (V*)out, a, t + ps.tw_off, t64 + ps.wc_off,
+                                                      t64 + ps.wf_off, scale);
+      CUDA_TRY(cudaGetLastError());
+      return 0;
+    }
+  }
   auto k = tfb::k_comb_tma<Real, L, INV, true, 0, F, IP>;
   if (int rc = ensure_smem((const void*)k, Cfg::SMEM)) return rc;
   int bps = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, Cfg::THREADS, Cfg::SMEM));
   const long long grid = std::max<long long>(1, std::min<long long>(a.ntiles, (long long)sm_count() * std::max(bps, 1)));
-  const V* t = (const V*)tb;
-  const double2* t64 = (const double2*)tb64;
   k<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, st>>>(map, (V*)out, a, t + ps.tw_off, t64 + ps.wc_off, t64 + ps.wf_off,
                                                      scale);
   CUDA_TRY(cudaGetLastError());
