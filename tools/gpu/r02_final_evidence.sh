@@ -23,7 +23,9 @@ prof() {
 prof rows_tma k_rows_tma 3 ""
 prof two_tma k_two_tma 1 "--config 2d_8192"
 prof rows_pf k_rows_pf 1 "--config 2d_8192"
-prof comb_2e26 k_comb_tma 2 "--config 1d_2e26"
+prof comb_2e26 k_comb_h3 2 "--config 1d_2e26"
+prof comb_2e30 k_comb_h3 0 "--config 1d_2e30"
 prof final_2e26 k_final_p 1 "--config 1d_2e26"
 prof final_2e30 k_final_p 0 "--config 1d_2e30"
+python tools/traffic_json.py gpurun_out/ev/bench_default.json gpurun_out/ev/launches > gpurun_out/ev/traffic.json
 du -sh gpurun_out/ev
