@@ -32,7 +32,7 @@ __device__ __forceinline__ void tstore(const CUtensorMap* m, int c0, int c1, con
 
 // tile t -> input (col chunk ci, row block); output tile position from its own map geometry
 __global__ void k_copy2(const __grid_constant__ CUtensorMap in, const __grid_constant__ CUtensorMap out, int R, int BR,
-                        int chunks_i, int chunks_o, long long ntiles, int tile_bytes) {
+                        int chunks_i, int chunks_o, long long ntiles, int tile_bytes, int F) {
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + tile_bytes);
   if (threadIdx.x != 0) return;
@@ -42,7 +42,7 @@ __global__ void k_copy2(const __grid_constant__ CUtensorMap in, const __grid_con
   auto issue = [&](long long t) {
     const int c = (int)(t % chunks_i), rb = (int)(t / chunks_i);
     mbar_expect(bar, tile_bytes);
-    for (int r = 0; r < R; r += BR) tload(sm + (size_t)r * 128, &in, c * 32, rb * R + r, bar);
+    for (int r = 0; r < R; r += BR) tload(sm + (size_t)r * F * 8, &in, c * 2 * F, rb * R + r, bar);
   };
   long long t = blockIdx.x;
   int k = 0;
@@ -50,7 +50,7 @@ __global__ void k_copy2(const __grid_constant__ CUtensorMap in, const __grid_con
   for (; t < ntiles; t += G, ++k) {
     mbar_wait(bar, k & 1);
     const int c = (int)(t % chunks_o), rb = (int)(t / chunks_o);
-    for (int r = 0; r < R; r += BR) tstore(&out, c * 32, rb * R + r, sm + (size_t)r * 128);
+    for (int r = 0; r < R; r += BR) tstore(&out, c * 2 * F, rb * R + r, sm + (size_t)r * F * 8);
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     if (t + G < ntiles) issue(t + G);
@@ -72,14 +72,17 @@ int main() {
   cudaMemset(a, 0, total * 8);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int R = 1024, BR = 256, tile_bytes = 16 * R * 8;
-  // widths (elements per row) of the read and the write layout; 16 = a tile is one contiguous 128 KB block
-  const long long W[][2] = {{1LL << 20, 1LL << 20}, {1024, 1024}, {1LL << 20, 16}, {1LL << 20, 1LL << 14},
-                            {1LL << 20, 1024}, {16, 1024}, {16, 16}, {1LL << 14, 1024}};
+  // {read width, write width, F}: widths in elements per row (F = contiguous tile = one 128 KB block);
+  // a tile is F adjacent columns (F * 8-byte lines) x 16384 / F rows = 128 KB
+  const long long W[][3] = {{1LL << 20, 1LL << 20, 16}, {1024, 1024, 16}, {1LL << 20, 16, 16}, {1LL << 20, 1LL << 14, 16},
+                            {1LL << 20, 1024, 16}, {16, 1024, 16}, {16, 16, 16}, {1LL << 14, 1024, 16},
+                            {16, 1LL << 20, 16}, {32, 1LL << 20, 32}, {1024, 1LL << 20, 16}, {1024, 1LL << 20, 32},
+                            {1LL << 20, 1LL << 20, 32}, {1024, 1024, 32}};
   auto E = enc();
   for (auto& w : W) {
+    const int F = (int)w[2], R = 16384 / F, BR = 256, tile_bytes = F * R * 8;
     CUtensorMap mi, mo;
-    cuuint32_t box[2] = {32, (cuuint32_t)BR};
+    cuuint32_t box[2] = {(cuuint32_t)(2 * F), (cuuint32_t)BR};
     cuuint32_t es[2] = {1, 1};
     cuuint64_t di[2] = {(cuuint64_t)w[0] * 2, (cuuint64_t)(total / w[0])}, si[1] = {(cuuint64_t)w[0] * 8};
     cuuint64_t dO[2] = {(cuuint64_t)w[1] * 2, (cuuint64_t)(total / w[1])}, so[1] = {(cuuint64_t)w[1] * 8};
@@ -89,22 +92,23 @@ int main() {
       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     const int smem = tile_bytes + 64;
     cudaFuncSetAttribute(k_copy2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int ci = (int)(w[0] / 16), co = (int)(w[1] / 16);
-    const long long ntiles = total / (16LL * R);
-    k_copy2<<<sms, 32, smem>>>(mi, mo, R, BR, ci, co, ntiles, tile_bytes);
+    const int ci = (int)(w[0] / F), co = (int)(w[1] / F);
+    const long long ntiles = total / (16384LL);
+    k_copy2<<<sms, 32, smem>>>(mi, mo, R, BR, ci, co, ntiles, tile_bytes, F);
     cudaDeviceSynchronize();
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int reps = 5;
     cudaEventRecord(e0);
-    for (int i = 0; i < reps; ++i) k_copy2<<<sms, 32, smem>>>(mi, mo, R, BR, ci, co, ntiles, tile_bytes);
+    for (int i = 0; i < reps; ++i) k_copy2<<<sms, 32, smem>>>(mi, mo, R, BR, ci, co, ntiles, tile_bytes, F);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    printf("read rows %8lld B apart, write rows %8lld B apart: %7.3f ms/pass %7.1f GB/s (r+w)  %s\n", w[0] * 8, w[1] * 8,
-           ms / reps, 2.0 * total * 8 * reps / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    printf("F %2d (%3d-byte lines): read rows %8lld B apart, write rows %8lld B apart: %7.3f ms/pass %7.1f GB/s (r+w)  %s\n",
+           F, F * 8, w[0] * 8, w[1] * 8, ms / reps, 2.0 * total * 8 * reps / (ms * 1e-3) / 1e9,
+           cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }
