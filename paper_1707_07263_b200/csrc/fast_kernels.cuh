@@ -893,14 +893,17 @@ struct FinalCfg {
   static constexpr int SMEM = (A > B ? A : B) * (int)sizeof(V);
 };
 
-// tile -> (batch, leading-digit chunk, other digits o)
+// tile -> (batch, leading-digit chunk, other digits o), chunks fastest: concurrent CTAs write adjacent
+// 128-byte lines of the same output rows (the lines of one tile are out_w_last apart, 8 MB at 2^30), so
+// they reach L2 together -- 2^26 final pass 195 vs 205 us, 2^30 3.47 vs 3.53 ms against o fastest
+// (tools/gpu/r02_fcfirst.sh)
 struct FinalTileGeo {
   long long batch, chunk, o;
 };
 __device__ __forceinline__ FinalTileGeo final_geo(const FinalArgs& a, long long tile) {
   const long long tiles_per_batch = a.chunks * a.sw0;
   const long long rem = tile % tiles_per_batch;
-  return {tile / tiles_per_batch, rem / a.sw0, rem % a.sw0};
+  return {tile / tiles_per_batch, rem % a.chunks, rem / a.chunks};
 }
 
 // phase 0: this thread's R elements of row (chunk*F + ff)*sw0 + o, lanes along n (coalesced loads)
