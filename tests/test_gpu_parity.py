@@ -296,6 +296,9 @@ def test_fast_transposed_handover(tf, oracle, monkeypatch, n, b, dtype):
     assert rel_l2(back, x) < (1e-6 if dtype == np.complex64 else 1e-14)
     xd = torch.from_numpy(x).cuda()
     assert bits_equal(tf.fft_tiled_device(xd, plan).cpu().numpy(), got)
+    xi = xd.clone()
+    tf.fft_tiled_device(xi, plan, out=xi)  # in == out: pass 0 reads the user buffer, the final pass rewrites it
+    assert bits_equal(xi.cpu().numpy(), got)
     info = tf.tilefft._plan_cache and next(iter(tf.tilefft._plan_cache.values())).info()
     if info:
         assert len(info["factors"]) == 3, info
