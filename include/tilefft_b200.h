@@ -106,7 +106,9 @@ typedef struct {
   uint32_t passes;             /* device passes per transform (HBM round trips) */
   uint64_t factors[16];        /* device pass lengths in execution order */
   uint32_t launches_per_exec;  /* kernel launches per tilefft_exec_c2c */
-  uint64_t workspace_bytes;    /* device scratch held by the plan */
+  uint64_t workspace_bytes;    /* device scratch held by the plan (FAST: n*batch elements for 2-pass plans,
+                                  2*n*batch for 3-pass plans, which hand over from pass 0 to pass 1 through a
+                                  second, transposed workspace) */
   uint64_t table_bytes;        /* device twiddle tables held by the plan */
 } tilefft_plan_info_t;
 TILEFFT_API int tilefft_plan_info(tilefft_plan_t plan, tilefft_plan_info_t* info);
