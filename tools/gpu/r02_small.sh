@@ -1,7 +1,10 @@
 #!/bin/bash
-# small (L2-resident) multi-pass plans: 4-comb/4-row tiles (default) vs the TMA in-place comb / persistent final
-for v in 1 2 3; do TILEFFT_NO_SMALL=$v timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "fast_mode_fp32 or inverse" 2>&1 | tail -1; done
-export CASE_TIMEOUT=60 REPS=500
-for i in 1 2; do
-python tools/gpu/two_probe.py '[["1d", 14], ["1d", 16], ["1d", 18], ["1d", 20], ["1d", 22]]' '[{}, {"TILEFFT_NO_SMALL": 1}, {"TILEFFT_NO_SMALL": 2}, {"TILEFFT_NO_SMALL": 3}]'
-done
+# 2^20 (L2 flushed per step) and 2^18 x 4: small-transform paths (4-comb tiles, k_final_t) vs 16-comb TMA tiles + k_final_p (TILEFFT_SMALL_OFF=1)
+mkdir -p gpurun_out
+for rep in 1 2; do
+for v in 0 1; do
+  TILEFFT_SMALL_OFF=$v timeout 300 python bench.py --configs 1d_2e20 --steps 200 --warmup 5 --no-cpu-baseline --no-cufft --e2e-steps 1 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1])
+r=d['configs']['1d_2e20']; print('SMALL_OFF=$v 1d_2e20', r['ms_per_step'], r['roofline'].get('pass_ms'), d['clocks']['sm_mhz'])"
+done; done
+CASE_TIMEOUT=60 REPS=200 python tools/gpu/two_probe.py '[["1d", 20], ["1d", 21], ["1d", 19]]' '[{"TILEFFT_SMALL_OFF": 0}, {"TILEFFT_SMALL_OFF": 1}, {"TILEFFT_SMALL_OFF": 0}, {"TILEFFT_SMALL_OFF": 1}]'
